@@ -1,0 +1,260 @@
+/* lshbeam_b200.h -- C ABI of the B200-native LSH beam-search hot path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no C++ or torch
+ * types. Each entry point names the reference interface it replaces
+ * (paths under /root/reference/proj). The C++ drop-in API in
+ * include/lshbeam/*.hpp (namespace lshbeam) is a thin layer over these
+ * calls, and INTEGRATION.md shows the ctypes / C++ bindings.
+ *
+ * Conventions
+ *  - Every call returns an lsb_status; lsb_last_error() gives a
+ *    thread-local message for the last failure on this thread.
+ *  - "_host" buffers are host memory (pageable or pinned); "_dev" buffers are
+ *    device pointers on the context's device. Stage entry points (section 3)
+ *    take host buffers and synchronise, like the reference's by-value API.
+ *    The fused step (section 4) is device-resident and asynchronous.
+ *  - Errors map to the reference's exceptions: LSB_EINVAL ~
+ *    std::invalid_argument, LSB_ERUNTIME ~ std::runtime_error.
+ *  - Matrices are dense row-major, as lshbeam::Mat<T>
+ *    (include/lshbeam/matrix.hpp:11-41); E is |V| x d
+ *    (include/lshbeam/model_provider.hpp:27).
+ */
+#ifndef LSHBEAM_B200_H
+#define LSHBEAM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSB_ABI_VERSION 1
+
+typedef enum lsb_status {
+  LSB_OK = 0,
+  LSB_EINVAL = 1,   /* bad shape / parameter / NaN input / sentinel key / T > V */
+  LSB_ERUNTIME = 2, /* cuckoo rebuild budget exhausted, empty candidate set */
+  LSB_ECUDA = 3,    /* CUDA runtime / launch failure */
+  LSB_ENOMEM = 4    /* device or pinned allocation failed */
+} lsb_status;
+
+/* Reduced-softmax arithmetic.
+ *  PARITY: FP32 multiplies and adds in the reference's exact order (4 SSE
+ *          lanes, no FMA; src/beam_decoder.cpp:34-42 as compiled by GCC -O3),
+ *          so logits, probabilities and chosen ids are bit-identical to the
+ *          CPU reference.
+ *  FAST:   FP32 FFMA in tile order; |dlogit| <= 1e-4 (1+|l|), ids exact
+ *          except at near-ties. */
+typedef enum lsb_mode { LSB_MODE_PARITY = 0, LSB_MODE_FAST = 1 } lsb_mode;
+
+/* One beam continuation, layout-compatible with lshbeam::BeamChoice
+ * (include/lshbeam/beam_decoder.hpp:22-26): score, source hypothesis, word
+ * (-1 = frozen hypothesis carried over). */
+typedef struct lsb_choice {
+  double score;
+  uint32_t beam;
+  uint32_t _pad;
+  int64_t word;
+} lsb_choice;
+
+typedef struct lsb_ctx lsb_ctx;     /* device + CUDA stream + error word  */
+typedef struct lsb_model lsb_model; /* device E (|V| x d fp32) + logit bias */
+typedef struct lsb_index lsb_index; /* device WTA perms + band index       */
+typedef struct lsb_batch lsb_batch; /* per-step scratch for S sentences   */
+
+/* ------------------------------------------------------------ 1. context */
+const char* lsb_last_error(void);
+int lsb_abi_version(void);
+/* stream: a cudaStream_t on `device`, or NULL to create a private
+ * non-blocking stream. */
+lsb_status lsb_ctx_create(int device, void* stream, lsb_ctx** out);
+lsb_status lsb_ctx_destroy(lsb_ctx* ctx);
+lsb_status lsb_ctx_sync(lsb_ctx* ctx);       /* sync + surface device errors */
+void* lsb_ctx_stream(lsb_ctx* ctx);          /* the cudaStream_t in use      */
+int lsb_ctx_device(lsb_ctx* ctx);
+int lsb_ctx_sm_count(lsb_ctx* ctx);
+/* Number of kernels this context has launched (for launch accounting). */
+uint64_t lsb_ctx_launch_count(lsb_ctx* ctx);
+
+/* -------------------------------------------------------------- 2. model
+ * Replaces holding SynthModel::embeddings / freq_bias in host memory
+ * (include/lshbeam/model_provider.hpp:21-32). E_host/bias_host are copied;
+ * bias_host may be NULL (all zero). */
+lsb_status lsb_model_create(lsb_ctx* ctx, const float* E_host, uint32_t vocab, int dim,
+                            const float* bias_host, lsb_model** out);
+/* Same, from device memory already on the context's device (copied). */
+lsb_status lsb_model_create_dev(lsb_ctx* ctx, const float* E_dev, uint32_t vocab, int dim,
+                                const float* bias_dev, lsb_model** out);
+lsb_status lsb_model_destroy(lsb_model* m);
+const float* lsb_model_embeddings_dev(const lsb_model* m);
+uint32_t lsb_model_vocab(const lsb_model* m);
+int lsb_model_dim(const lsb_model* m);
+
+/* -------------------------------------------------------------- 3. index */
+
+/* Replaces build_lsh_index(E, WtaParams{K,u,W,perm_seed}, index_seed)
+ * (src/band_index.cpp:189-196): permutations on the host (bit-exact
+ * SplitMix64 Fisher-Yates, src/wta_hash.cpp:31-55), WTA hash of E (K1), then
+ * per band the stable (code, id) sort, spans and the parallel cuckoo build
+ * (K2-build). LSB_EINVAL on bad {K,u,W} or NaN in E; LSB_ERUNTIME if a
+ * band's cuckoo build exhausts the rebuild budget. */
+lsb_status lsb_index_build(lsb_ctx* ctx, const lsb_model* model, int K, int u, int W,
+                           uint64_t perm_seed, uint64_t index_seed, lsb_index** out);
+/* Replaces BandIndex::build(band_codes, seed) (src/band_index.cpp:90-132) for a
+ * host |V| x W code matrix (no permutations attached: step calls need an
+ * index from lsb_index_build). */
+lsb_status lsb_index_build_codes(lsb_ctx* ctx, const uint32_t* codes_host, uint32_t vocab,
+                                 int W, uint64_t index_seed, lsb_index** out);
+lsb_status lsb_index_destroy(lsb_index* idx);
+
+typedef struct lsb_index_info {
+  uint32_t vocab;
+  int W, K, u, bits_per_index, dim;
+  uint64_t perm_seed, index_seed;
+  uint32_t max_span;      /* BandIndex::max_span_length (band_index.cpp:177-183) */
+  uint32_t build_attempts;/* cuckoo attempts used by the worst band (1 = first) */
+} lsb_index_info;
+lsb_status lsb_index_info_get(const lsb_index* idx, lsb_index_info* out);
+/* Band w as the reference exposes it: band_words(w) (V ids), the table's
+ * log2 capacity, multipliers and 2*2^lg slots as (key, start, length)
+ * triples (BandIndex::band_words / CuckooTable::slots). Any output may be
+ * NULL; *lg is always written. Slot placement is the GPU build's; spans are
+ * identical to the reference's. */
+lsb_status lsb_index_band(const lsb_index* idx, int w, uint32_t* word_ids_host,
+                          uint32_t* lg, uint64_t* mul2, uint32_t* slots_host);
+/* CuckooTable::find for a batch of (band, key) queries, on the device:
+ * found[i] = 1 and (start,len) on a hit (band_index.cpp:73-88). */
+lsb_status lsb_index_find(lsb_ctx* ctx, const lsb_index* idx, const int32_t* bands_host,
+                          const uint32_t* keys_host, size_t n, uint32_t* start_host,
+                          uint32_t* len_host, uint8_t* found_host);
+/* Permutation prefixes (u*W x K) of the index, as generated. */
+lsb_status lsb_index_perms(const lsb_index* idx, uint32_t* perms_host);
+
+/* -------------------------------------------- 4. stage entry points (host)
+ * Each mirrors one reference function; used by the C++ drop-in layer and
+ * the per-stage parity tests. Synchronous. */
+
+/* hash_matrix(M, perms, params) (src/wta_hash.cpp:147-171): n x d rows ->
+ * n x W band codes; perms_host is (u*W) x K prefixes. NaN -> LSB_EINVAL. */
+lsb_status lsb_wta_hash(lsb_ctx* ctx, const float* M_host, int64_t n, int d,
+                        const uint32_t* perms_host, int K, int u, int W,
+                        uint32_t* codes_host);
+/* BandIndex::lookup_hits_into(query_codes, L) (src/band_index.cpp:134-162):
+ * dense B x V int32 hit counts. */
+lsb_status lsb_lookup_hits(lsb_ctx* ctx, const lsb_index* idx, const uint32_t* q_host,
+                           int B, int32_t* L_host);
+/* select_candidates(L, t) (src/candidate_selector.cpp:14-55). ids_host has
+ * room for V ids. */
+lsb_status lsb_select_candidates(lsb_ctx* ctx, const int32_t* L_host, int B, uint32_t V,
+                                 int t, uint32_t* ids_host, uint32_t* n_out,
+                                 uint32_t* from_threshold);
+/* merge_top_frequent(cands, T, specials, V) (src/candidate_selector.cpp:57-103).
+ * out_host has room for n + T + nspec ids; prov = {from_threshold,
+ * from_top, from_specials}. */
+lsb_status lsb_merge_top_frequent(lsb_ctx* ctx, const uint32_t* ids_host, uint32_t n,
+                                  uint32_t from_threshold, uint32_t T,
+                                  const uint32_t* specials_host, uint32_t nspec, uint32_t V,
+                                  uint32_t* out_host, uint32_t* n_out, uint32_t* prov);
+/* gather_embeddings(E, cands) (src/candidate_selector.cpp:105-119). */
+lsb_status lsb_gather_embeddings(lsb_ctx* ctx, const lsb_model* model,
+                                 const uint32_t* ids_host, uint32_t n, float* out_host);
+/* compute_logits(H, E_sub) (src/beam_decoder.cpp:23-44): rows x n logits. */
+lsb_status lsb_compute_logits(lsb_ctx* ctx, const float* H_host, int rows,
+                              const float* Esub_host, int64_t n, int d, lsb_mode mode,
+                              float* out_host);
+/* softmax_rows(logits) (src/beam_decoder.cpp:46-74). A row with no finite
+ * entry (or n == 0) -> LSB_EINVAL. */
+lsb_status lsb_softmax_rows(lsb_ctx* ctx, const float* logits_host, int rows, int64_t n,
+                            float* out_host);
+/* expand_beams(probs, cum, live, frozen, B, id_map) (src/beam_decoder.cpp:76-111).
+ * id_map_host may be NULL (identity). frozen entries use word = -1.
+ * out_host has room for B choices. */
+lsb_status lsb_expand_beams(lsb_ctx* ctx, const float* probs_host, int rows, int64_t n,
+                            const double* cum_host, const uint32_t* live_host,
+                            const lsb_choice* frozen_host, int nfrozen, int B,
+                            const uint32_t* id_map_host, lsb_choice* out_host, int* n_out);
+
+/* --------------------------------------- 5. fused per-step pipeline (device)
+ * One decode step of S independent sentences, each holding up to B
+ * hypotheses: the kLsh branch of decode() plus expansion
+ * (src/beam_decoder.cpp:166-289), batched. Per sentence s the state mirrors
+ * decode()'s `hyps` vector: hypotheses 0..n_hyp[s]-1 with cumulative score,
+ * finished flag and hidden vector; live = unfinished (in index order),
+ * frozen = finished (they compete with their carried score).
+ *
+ * K1+K2 (hash + cuckoo probe + hit count, vocab-tiled smem counters) ->
+ * K3 (threshold bitmap U top-T U specials, ascending compaction) ->
+ * K4 (H . E_LSH^T + bias, shared top-T block + per-sentence survivors) ->
+ * K5 (row softmax, per-row top-B, per-sentence top-B merge, hidden reorder).
+ * No host synchronisation; errors surface at the next lsb_ctx_sync. */
+typedef struct lsb_step_config {
+  int S;                    /* sentences per batch                        */
+  int B;                    /* beam width (hypothesis slots per sentence) */
+  uint32_t top_merge;       /* T                                          */
+  int threshold;            /* t (0 = whole vocabulary)                   */
+  const uint32_t* specials; /* host ids always kept (decode adds EOS)     */
+  int nspec;
+  lsb_mode mode;
+  int full_vocab;           /* 1 = kFull: score all of V, no LSH stages   */
+} lsb_step_config;
+
+/* Validates like DecodeConfig::validate (src/candidate_selector.cpp:121-132). */
+lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_index* idx,
+                            const lsb_step_config* cfg, lsb_batch** out);
+lsb_status lsb_batch_destroy(lsb_batch* b);
+
+typedef struct lsb_state_dev {
+  const float* hidden;      /* [S][B][d]  hypothesis hidden vectors */
+  const double* scores;     /* [S][B]     cumulative log-prob       */
+  const uint8_t* finished;  /* [S][B]     1 = frozen                */
+  const int32_t* n_hyp;     /* [S]        live+frozen hypotheses    */
+} lsb_state_dev;
+
+typedef struct lsb_out_dev {
+  lsb_choice* choices;      /* [S][B]                                   */
+  int32_t* n_choices;       /* [S]                                      */
+  float* hidden_out;        /* [S][B][d] parent rows (reorder) or NULL  */
+} lsb_out_dev;
+
+lsb_status lsb_step(lsb_batch* b, const lsb_state_dev* in, const lsb_out_dev* out);
+
+/* End-to-end variant for host-resident state (pinned or pageable): copies
+ * the state in, runs lsb_step, copies choices/n_choices (and hidden_out if
+ * non-NULL) back, synchronises and surfaces errors. */
+typedef struct lsb_state_host {
+  const float* hidden;
+  const double* scores;
+  const uint8_t* finished;
+  const int32_t* n_hyp;
+} lsb_state_host;
+lsb_status lsb_step_host(lsb_batch* b, const lsb_state_host* in, lsb_choice* choices_host,
+                         int32_t* n_choices_host, float* hidden_out_host);
+
+/* Per-sentence views of the last step (device -> host copies, synchronous):
+ * candidate ids (|V_LSH| of them, ascending), provenance
+ * {from_threshold, from_top, from_specials}, query band codes
+ * ([B][W], live rows only), and probabilities over the candidates for each
+ * live row ([n_live][n_cand]). */
+lsb_status lsb_batch_candidates(lsb_batch* b, int s, uint32_t* ids_host, uint32_t* n_cand,
+                                uint32_t* prov3);
+lsb_status lsb_batch_query_codes(lsb_batch* b, int s, uint32_t* codes_host);
+lsb_status lsb_batch_probs(lsb_batch* b, int s, float* probs_host, int* n_live);
+/* Device pointer to the last step's per-sentence candidate counts [S]. */
+const uint32_t* lsb_batch_n_cand_dev(lsb_batch* b);
+/* Keep probabilities of every live row after a step (default off: the step
+ * then writes only what the top-B selection needs). */
+lsb_status lsb_batch_keep_probs(lsb_batch* b, int on);
+
+/* Per-kernel device time, milliseconds, measured with CUDA events recorded
+ * on the context stream between the step's kernels when profiling is on:
+ * [probe_count, compact, logits, softmax_topb, expand]. stage_ms: last step;
+ * stage_totals: sum over the steps since the previous call (<= 1024). */
+lsb_status lsb_batch_profile(lsb_batch* b, int on);
+lsb_status lsb_batch_stage_ms(lsb_batch* b, float* ms5);
+lsb_status lsb_batch_stage_totals(lsb_batch* b, float* ms5, int* nsteps);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSHBEAM_B200_H */

@@ -1,0 +1,416 @@
+// capi_step.cu -- the fused per-step pipeline (lsb_batch / lsb_step).
+//
+// One call = one decode step of S sentences: decode()'s kLsh branch plus
+// expand_beams (src/beam_decoder.cpp:200-289), batched over sentences, all on
+// the context stream with no host synchronisation:
+//   K1+K2 k_probe_count -> K3 k_compact -> K4 k_logits -> K5a k_softmax_topb
+//   -> K5b k_expand.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "k_step.cuh"
+
+using namespace lsb;
+
+struct lsb_batch {
+  lsb_ctx* ctx = nullptr;
+  const lsb_model* model = nullptr;
+  const lsb_index* idx = nullptr;
+  int S = 0, B = 0, d = 0, t = 0;
+  uint32_t V = 0, T = 0;
+  lsb_mode mode = LSB_MODE_PARITY;
+  int cmode = 0;  // 0 threshold, 1 all words (t == 0), 2 full vocabulary
+  uint32_t n_shared = 0;
+  size_t ncap = 0;
+  uint32_t nwords = 0, slice_len = 0;
+  int counter_bytes = 1;
+  int nspec = 0;
+  int keep_probs = 0;
+  // device scratch
+  uint32_t* specials = nullptr;
+  uint32_t* qcodes = nullptr;
+  uint32_t* bitmap = nullptr;
+  uint32_t* ids = nullptr;
+  uint32_t* n_cand = nullptr;
+  uint32_t* prov = nullptr;
+  float* logits = nullptr;
+  TopEntry* top = nullptr;
+  int32_t* top_n = nullptr;
+  // staging for lsb_step_host
+  float* h_hidden = nullptr;
+  double* h_scores = nullptr;
+  uint8_t* h_finished = nullptr;
+  int32_t* h_nhyp = nullptr;
+  lsb_choice* h_choices = nullptr;
+  int32_t* h_nchoices = nullptr;
+  float* h_hidden_out = nullptr;
+  // last step (for the per-sentence views)
+  lsb_state_dev last{};
+  bool has_last = false;
+  // profiling: one set of 6 events per step in a ring, summed on demand
+  bool profile = false;
+  std::vector<cudaEvent_t> ring;  // kRing * 6
+  int ring_next = 0, ring_used = 0;
+  cudaEvent_t* ev = nullptr;       // current step's 6 events
+};
+
+static constexpr int kRing = 1024;
+
+namespace {
+
+template <class T>
+cudaError_t dalloc(T** p, size_t n) {
+  return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T));
+}
+
+lsb_status free_batch(lsb_batch* b) {
+  if (!b) return LSB_OK;
+  void* ptrs[] = {b->specials, b->qcodes,   b->bitmap,     b->ids,          b->n_cand,
+                  b->prov,     b->logits,   b->top,        b->top_n,        b->h_hidden,
+                  b->h_scores, b->h_finished, b->h_nhyp,   b->h_choices,    b->h_nchoices,
+                  b->h_hidden_out};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto& e : b->ring)
+    if (e) cudaEventDestroy(e);
+  delete b;
+  return LSB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_index* idx,
+                            const lsb_step_config* cfg, lsb_batch** out) {
+  if (!ctx || !model || !cfg || !out) return set_error("lsb_batch_create: null argument"), LSB_EINVAL;
+  *out = nullptr;
+  const uint32_t V = model->V;
+  // DecodeConfig::validate (src/candidate_selector.cpp:121-132)
+  if (cfg->B < 1) return set_error("config: beam must be >= 1"), LSB_EINVAL;
+  if (cfg->B > 64) return set_error("config: beam above 64 is not supported by the fused step"), LSB_EINVAL;
+  if (cfg->S < 1) return set_error("config: at least one sentence"), LSB_EINVAL;
+  if (cfg->top_merge > V) return set_error("config: T exceeds vocabulary size"), LSB_EINVAL;
+  if (!cfg->full_vocab) {
+    if (!idx || !idx->has_perms)
+      return set_error("decode: lsh mode requires an index"), LSB_EINVAL;
+    if (idx->V != V || idx->dim != model->d)
+      return set_error("decode: index does not match the model"), LSB_EINVAL;
+    if (cfg->threshold < 0 || cfg->threshold > idx->W)
+      return set_error("config: t must be in [0, W]"), LSB_EINVAL;
+  }
+  std::vector<uint32_t> spec(cfg->specials, cfg->specials + std::max(0, cfg->nspec));
+  for (uint32_t id : spec)
+    if (id >= V) return set_error("config: special id out of range"), LSB_EINVAL;
+  std::sort(spec.begin(), spec.end());
+  spec.erase(std::unique(spec.begin(), spec.end()), spec.end());
+  LSB_CUDA(cudaSetDevice(ctx->device));
+
+  auto* b = new lsb_batch;
+  b->ctx = ctx;
+  b->model = model;
+  b->idx = cfg->full_vocab ? nullptr : idx;
+  b->S = cfg->S;
+  b->B = cfg->B;
+  b->d = model->d;
+  b->V = V;
+  b->T = cfg->top_merge;
+  b->t = cfg->threshold;
+  b->mode = cfg->mode;
+  b->cmode = cfg->full_vocab ? 2 : (cfg->threshold == 0 ? 1 : 0);
+  b->n_shared = b->cmode ? V : b->T;
+  b->ncap = (static_cast<size_t>(V) + 3) & ~size_t(3);
+  b->nwords = (V + 31) / 32;
+  b->nspec = static_cast<int>(spec.size());
+  if (b->idx) {
+    b->counter_bytes = b->idx->W < 256 ? 1 : 2;
+    const uint32_t budget = 96 * 1024 / b->counter_bytes;
+    const uint32_t nslices = (V + budget - 1) / budget;
+    b->slice_len = ((V + nslices - 1) / nslices + 63) & ~63u;
+  }
+  const size_t SB = static_cast<size_t>(b->S) * b->B;
+  cudaError_t e = dalloc(&b->specials, spec.size());
+  if (e == cudaSuccess && !spec.empty())
+    e = cudaMemcpy(b->specials, spec.data(), spec.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = dalloc(&b->qcodes, SB * (b->idx ? b->idx->W : 1));
+  if (e == cudaSuccess) e = dalloc(&b->bitmap, static_cast<size_t>(b->S) * b->nwords);
+  if (e == cudaSuccess)
+    e = cudaMemset(b->bitmap, 0, std::max<size_t>(1, static_cast<size_t>(b->S) * b->nwords) * 4);
+  if (e == cudaSuccess) e = dalloc(&b->ids, static_cast<size_t>(b->S) * b->ncap);
+  if (e == cudaSuccess) e = dalloc(&b->n_cand, b->S);
+  if (e == cudaSuccess) e = dalloc(&b->prov, 3 * b->S);
+  if (e == cudaSuccess) e = dalloc(&b->logits, SB * b->ncap);
+  if (e == cudaSuccess) e = dalloc(&b->top, SB * b->B);
+  if (e == cudaSuccess) e = dalloc(&b->top_n, SB);
+  if (e != cudaSuccess) {
+    free_batch(b);
+    return cuda_status(e, "lsb_batch_create");
+  }
+  *out = b;
+  return LSB_OK;
+}
+
+lsb_status lsb_batch_destroy(lsb_batch* b) {
+  if (b && b->ctx) cudaStreamSynchronize(b->ctx->stream);
+  return free_batch(b);
+}
+
+lsb_status lsb_batch_keep_probs(lsb_batch* b, int on) {
+  if (!b) return LSB_EINVAL;
+  b->keep_probs = on ? 1 : 0;
+  return LSB_OK;
+}
+
+lsb_status lsb_batch_profile(lsb_batch* b, int on) {
+  if (!b) return LSB_EINVAL;
+  if (on && b->ring.empty()) {
+    b->ring.assign(kRing * 6, nullptr);
+    for (auto& e : b->ring) LSB_CUDA(cudaEventCreate(&e));
+  }
+  b->profile = on != 0;
+  b->ring_next = b->ring_used = 0;
+  return LSB_OK;
+}
+
+// Sums the per-stage device time of the steps recorded since the last call
+// (at most the last kRing steps) and restarts the ring.
+lsb_status lsb_batch_stage_totals(lsb_batch* b, float* ms5, int* nsteps) {
+  if (!b || !ms5) return LSB_EINVAL;
+  if (!b->profile) return set_error("profiling is off"), LSB_EINVAL;
+  for (int k = 0; k < 5; ++k) ms5[k] = 0.0f;
+  const int n = std::min(b->ring_used, kRing);
+  for (int i = 0; i < n; ++i) {
+    cudaEvent_t* ev = &b->ring[static_cast<size_t>(i) * 6];
+    LSB_CUDA(cudaEventSynchronize(ev[5]));
+    for (int k = 0; k < 5; ++k) {
+      float ms = 0.0f;
+      LSB_CUDA(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+      ms5[k] += ms;
+    }
+  }
+  if (nsteps) *nsteps = n;
+  b->ring_next = b->ring_used = 0;
+  return LSB_OK;
+}
+
+lsb_status lsb_batch_stage_ms(lsb_batch* b, float* ms5) {
+  if (!b || !ms5) return LSB_EINVAL;
+  if (!b->profile || !b->ring_used) return set_error("profiling is off"), LSB_EINVAL;
+  const int last = (b->ring_next + kRing - 1) % kRing;
+  cudaEvent_t* ev = &b->ring[static_cast<size_t>(last) * 6];
+  LSB_CUDA(cudaEventSynchronize(ev[5]));
+  for (int k = 0; k < 5; ++k) LSB_CUDA(cudaEventElapsedTime(&ms5[k], ev[k], ev[k + 1]));
+  return LSB_OK;
+}
+
+lsb_status lsb_step(lsb_batch* b, const lsb_state_dev* in, const lsb_out_dev* out) {
+  if (!b || !in || !out || !in->hidden || !in->scores || !out->choices || !out->n_choices)
+    return set_error("lsb_step: null argument"), LSB_EINVAL;
+  lsb_ctx* ctx = b->ctx;
+  cudaStream_t st = ctx->stream;
+  const int R = b->S * b->B;
+  lsb_status rc;
+  if (b->profile) {
+    b->ev = &b->ring[static_cast<size_t>(b->ring_next) * 6];
+    b->ring_next = (b->ring_next + 1) % kRing;
+    b->ring_used = std::min(b->ring_used + 1, kRing);
+    LSB_CUDA(cudaEventRecord(b->ev[0], st));
+  }
+  // K1 + K2
+  if (b->cmode != 2) {
+    ProbeArgs pa{};
+    pa.ix = b->idx->view();
+    pa.hidden = in->hidden;
+    pa.finished = in->finished;
+    pa.n_hyp = in->n_hyp;
+    pa.S = b->S;
+    pa.B = b->B;
+    pa.t = b->t;
+    pa.slice_len = b->slice_len;
+    pa.counter_bytes = b->counter_bytes;
+    pa.qcodes = b->qcodes;
+    pa.bitmap = b->bitmap;
+    pa.nwords = b->nwords;
+    pa.err = ctx->err_dev;
+    if ((rc = launch_probe(ctx, pa))) return rc;
+  }
+  if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[1], st));
+  // K3
+  CompactArgs ca{};
+  ca.bitmap_in = b->bitmap;
+  ca.bitmap_clear = b->bitmap;
+  ca.nwords = b->nwords;
+  ca.V = b->V;
+  ca.T = b->T;
+  ca.mode = b->cmode;
+  ca.specials = b->specials;
+  ca.nspec = b->nspec;
+  ca.ids = b->ids;
+  ca.ncap = b->ncap;
+  ca.n_cand = b->n_cand;
+  ca.prov = b->prov;
+  ca.empty_is_error = 1;
+  ca.n_hyp = in->n_hyp;
+  ca.finished = in->finished;
+  ca.B = b->B;
+  ca.err = ctx->err_dev;
+  if ((rc = launch_compact(ctx, ca, b->S))) return rc;
+  if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[2], st));
+  // K4
+  LogitsArgs la{};
+  la.H = in->hidden;
+  la.d = b->d;
+  la.R_total = R;
+  la.Bsent = b->B;
+  la.E = b->model->E;
+  la.bias = b->model->bias;
+  la.n_shared = b->n_shared;
+  la.ids = b->cmode == 0 ? b->ids : nullptr;
+  la.ncap = b->ncap;
+  la.n_cand = b->n_cand;
+  la.S = b->S;
+  la.out = b->logits;
+  la.ldo = b->ncap;
+  if ((rc = launch_logits(ctx, la, b->mode, ctx->sm_count * 8))) return rc;
+  if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[3], st));
+  // K5a
+  SoftmaxArgs sa{};
+  sa.logits = b->logits;
+  sa.ldl = b->ncap;
+  sa.R_total = R;
+  sa.Bsent = b->B;
+  sa.topB = b->B;
+  sa.n_cand = b->n_cand;
+  sa.finished = in->finished;
+  sa.n_hyp = in->n_hyp;
+  sa.keep_probs = b->keep_probs;
+  sa.top = b->top;
+  sa.top_n = b->top_n;
+  sa.err = ctx->err_dev;
+  if ((rc = launch_softmax(ctx, sa))) return rc;
+  if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[4], st));
+  // K5b
+  ExpandArgs ea{};
+  ea.S = b->S;
+  ea.Bsent = b->B;
+  ea.topB = b->B;
+  ea.top = b->top;
+  ea.top_n = b->top_n;
+  ea.scores = in->scores;
+  ea.finished = in->finished;
+  ea.n_hyp = in->n_hyp;
+  ea.ids = b->cmode == 0 ? b->ids : nullptr;
+  ea.ncap = b->ncap;
+  ea.n_shared = b->n_shared;
+  ea.hidden = in->hidden;
+  ea.d = b->d;
+  ea.hidden_out = out->hidden_out;
+  ea.choices = out->choices;
+  ea.n_choices = out->n_choices;
+  if ((rc = launch_expand(ctx, ea))) return rc;
+  if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[5], st));
+  b->last = *in;
+  b->has_last = true;
+  return LSB_OK;
+}
+
+lsb_status lsb_step_host(lsb_batch* b, const lsb_state_host* in, lsb_choice* choices_host,
+                         int32_t* n_choices_host, float* hidden_out_host) {
+  if (!b || !in || !in->hidden || !in->scores || !choices_host || !n_choices_host)
+    return set_error("lsb_step_host: null argument"), LSB_EINVAL;
+  const size_t SB = static_cast<size_t>(b->S) * b->B;
+  const size_t HD = SB * b->d;
+  cudaStream_t st = b->ctx->stream;
+  if (!b->h_hidden) {
+    LSB_CUDA(dalloc(&b->h_hidden, HD));
+    LSB_CUDA(dalloc(&b->h_scores, SB));
+    LSB_CUDA(dalloc(&b->h_finished, SB));
+    LSB_CUDA(dalloc(&b->h_nhyp, b->S));
+    LSB_CUDA(dalloc(&b->h_choices, SB));
+    LSB_CUDA(dalloc(&b->h_nchoices, b->S));
+  }
+  if (hidden_out_host && !b->h_hidden_out) LSB_CUDA(dalloc(&b->h_hidden_out, HD));
+  LSB_CUDA(cudaMemcpyAsync(b->h_hidden, in->hidden, HD * 4, cudaMemcpyHostToDevice, st));
+  LSB_CUDA(cudaMemcpyAsync(b->h_scores, in->scores, SB * 8, cudaMemcpyHostToDevice, st));
+  lsb_state_dev d{};
+  d.hidden = b->h_hidden;
+  d.scores = b->h_scores;
+  if (in->finished) {
+    LSB_CUDA(cudaMemcpyAsync(b->h_finished, in->finished, SB, cudaMemcpyHostToDevice, st));
+    d.finished = b->h_finished;
+  }
+  if (in->n_hyp) {
+    LSB_CUDA(cudaMemcpyAsync(b->h_nhyp, in->n_hyp, b->S * 4, cudaMemcpyHostToDevice, st));
+    d.n_hyp = b->h_nhyp;
+  }
+  lsb_out_dev o{};
+  o.choices = b->h_choices;
+  o.n_choices = b->h_nchoices;
+  o.hidden_out = hidden_out_host ? b->h_hidden_out : nullptr;
+  lsb_status rc = lsb_step(b, &d, &o);
+  if (rc) return rc;
+  LSB_CUDA(cudaMemcpyAsync(choices_host, b->h_choices, SB * sizeof(lsb_choice),
+                           cudaMemcpyDeviceToHost, st));
+  LSB_CUDA(cudaMemcpyAsync(n_choices_host, b->h_nchoices, b->S * 4, cudaMemcpyDeviceToHost, st));
+  if (hidden_out_host)
+    LSB_CUDA(cudaMemcpyAsync(hidden_out_host, b->h_hidden_out, HD * 4, cudaMemcpyDeviceToHost, st));
+  return lsb_ctx_sync(b->ctx);
+}
+
+lsb_status lsb_batch_candidates(lsb_batch* b, int s, uint32_t* ids_host, uint32_t* n_cand,
+                                uint32_t* prov3) {
+  if (!b || s < 0 || s >= b->S || !n_cand) return set_error("lsb_batch_candidates: bad sentence"), LSB_EINVAL;
+  cudaStream_t st = b->ctx->stream;
+  uint32_t prov[3];
+  LSB_CUDA(cudaMemcpyAsync(n_cand, b->n_cand + s, 4, cudaMemcpyDeviceToHost, st));
+  LSB_CUDA(cudaMemcpyAsync(prov, b->prov + 3 * s, 12, cudaMemcpyDeviceToHost, st));
+  LSB_CUDA(cudaStreamSynchronize(st));
+  if (prov3) std::memcpy(prov3, prov, 12);
+  if (ids_host) {
+    if (b->cmode == 0) {
+      LSB_CUDA(cudaMemcpy(ids_host, b->ids + static_cast<size_t>(s) * b->ncap, *n_cand * 4ull,
+                          cudaMemcpyDeviceToHost));
+    } else {
+      for (uint32_t r = 0; r < *n_cand; ++r) ids_host[r] = r;
+    }
+  }
+  return LSB_OK;
+}
+
+lsb_status lsb_batch_query_codes(lsb_batch* b, int s, uint32_t* codes_host) {
+  if (!b || !b->idx || s < 0 || s >= b->S) return set_error("lsb_batch_query_codes: bad sentence"), LSB_EINVAL;
+  const size_t n = static_cast<size_t>(b->B) * b->idx->W;
+  LSB_CUDA(cudaMemcpy(codes_host, b->qcodes + s * n, n * 4, cudaMemcpyDeviceToHost));
+  return LSB_OK;
+}
+
+lsb_status lsb_batch_probs(lsb_batch* b, int s, float* probs_host, int* n_live) {
+  if (!b || s < 0 || s >= b->S || !b->has_last) return set_error("lsb_batch_probs: no step"), LSB_EINVAL;
+  if (!b->keep_probs) return set_error("lsb_batch_probs: enable lsb_batch_keep_probs first"), LSB_EINVAL;
+  cudaStream_t st = b->ctx->stream;
+  LSB_CUDA(cudaStreamSynchronize(st));
+  uint32_t n = 0;
+  int32_t nh = b->B;
+  std::vector<uint8_t> fin(b->B, 0);
+  LSB_CUDA(cudaMemcpy(&n, b->n_cand + s, 4, cudaMemcpyDeviceToHost));
+  if (b->last.n_hyp) LSB_CUDA(cudaMemcpy(&nh, b->last.n_hyp + s, 4, cudaMemcpyDeviceToHost));
+  if (b->last.finished)
+    LSB_CUDA(cudaMemcpy(fin.data(), b->last.finished + static_cast<size_t>(s) * b->B, b->B,
+                        cudaMemcpyDeviceToHost));
+  int live = 0;
+  for (int i = 0; i < nh; ++i) {
+    if (fin[i]) continue;
+    if (probs_host)
+      LSB_CUDA(cudaMemcpy(probs_host + static_cast<size_t>(live) * n,
+                          b->logits + (static_cast<size_t>(s) * b->B + i) * b->ncap, n * 4ull,
+                          cudaMemcpyDeviceToHost));
+    ++live;
+  }
+  if (n_live) *n_live = live;
+  return LSB_OK;
+}
+
+const uint32_t* lsb_batch_n_cand_dev(lsb_batch* b) { return b ? b->n_cand : nullptr; }
+
+}  // extern "C"

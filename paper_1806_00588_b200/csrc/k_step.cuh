@@ -1,0 +1,122 @@
+// k_step.cuh -- kernel argument blocks and launch helpers shared by the
+// fused step (capi_step.cu) and the per-stage entry points (capi_stages.cu).
+#pragma once
+
+#include "lsb_internal.cuh"
+
+namespace lsb {
+
+struct TopEntry {
+  float p;     // probability
+  uint32_t r;  // candidate column
+};
+
+// K1+K2: hash + probe + threshold hit counting.
+struct ProbeArgs {
+  IndexView ix;
+  const float* hidden;      // [S*B][d]
+  const uint8_t* finished;  // [S*B] or null (all live)
+  const int32_t* n_hyp;     // [S] or null (all B)
+  int S, B, t;
+  uint32_t slice_len;       // counters per CTA (multiple of 64)
+  int counter_bytes;        // 1 or 2
+  uint32_t* qcodes;         // [S*B][W]
+  uint32_t* bitmap;         // [S][nwords]
+  uint32_t nwords;
+  uint32_t* err;
+};
+
+// K3: bitmap (threshold survivors) U [0,T) U specials -> ascending ids.
+struct CompactArgs {
+  const uint32_t* bitmap_in;  // [S][nwords] or null (ids-from-list mode)
+  uint32_t* bitmap_clear;     // cleared after reading (may equal bitmap_in)
+  uint32_t nwords, V, T;
+  int mode;                   // 0 threshold, 1 all (t == 0), 2 full vocab
+  const uint32_t* specials;   // sorted unique, < V
+  int nspec;
+  uint32_t* ids;              // [S][ncap]
+  size_t ncap;
+  uint32_t* n_cand;           // [S]
+  uint32_t* prov;             // [S][3]
+  int empty_is_error;         // decode(): an empty set with live rows throws
+  const int32_t* n_hyp;       // live check for the empty-set error (may be null)
+  const uint8_t* finished;
+  int B;
+  uint32_t* err;
+};
+
+// K4: logits = H . E[ids]^T + bias[ids].
+struct LogitsArgs {
+  const float* H;          // [R_total][d]
+  int d, R_total, Bsent;   // rows per sentence for the per-sentence jobs
+  const float* E;          // [V][d]
+  const float* bias;       // [V] or null
+  uint32_t n_shared;       // columns [0, n_shared) use identity ids
+  const uint32_t* ids;     // [S][ncap]
+  size_t ncap;
+  const uint32_t* n_cand;  // [S]
+  int S, G, X;
+  int jobs_shared, ctiles_shared;
+  float* out;              // [R_total][ldo]
+  size_t ldo;
+};
+
+// K5a: row softmax + per-row top-B by (p desc, column asc).
+struct SoftmaxArgs {
+  float* logits;           // [R_total][ldl], overwritten with exp / probs
+  size_t ldl;
+  int R_total, Bsent, topB;
+  const uint32_t* n_cand;  // [S], or null: every row has n_const columns
+  uint32_t n_const;
+  int probs_in;            // 1: logits already hold probabilities (selection only)
+  const uint8_t* finished; // may be null
+  const int32_t* n_hyp;    // may be null
+  int keep_probs;
+  TopEntry* top;           // [R_total][topB]
+  int32_t* top_n;          // [R_total]
+  uint32_t* err;
+};
+
+// K5b: per-sentence top-B merge by (score desc, beam asc, word asc) +
+// hidden-state reorder.
+struct ExpandArgs {
+  int S, Bsent, topB;
+  const TopEntry* top;
+  const int32_t* top_n;
+  const double* scores;     // [S][Bsent] cumulative, per hypothesis
+  const uint8_t* finished;  // [S][Bsent] or null
+  const int32_t* n_hyp;     // [S] or null
+  const uint32_t* live_ids; // [S][Bsent] beam id of live row i, or null (= i)
+  const uint32_t* ids;      // [S][ncap]
+  size_t ncap;
+  uint32_t n_shared;
+  const uint32_t* id_map;   // optional global id map (stage API), else ids
+  const float* hidden;      // [S][Bsent][d] parent rows by hypothesis, or null
+  int d;
+  float* hidden_out;        // [S][Bsent][d] or null
+  lsb_choice* choices;      // [S][Bsent]
+  int32_t* n_choices;       // [S]
+  int frozen_mode;          // 0 = frozen from finished flags, 1 = explicit list
+  const double* fz_score;   // explicit frozen list (stage API)
+  const uint32_t* fz_beam;
+  int nfrozen;
+};
+
+lsb_status launch_probe(lsb_ctx* ctx, const ProbeArgs& a);
+lsb_status launch_compact(lsb_ctx* ctx, const CompactArgs& a, int S);
+lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_ctas);
+lsb_status launch_softmax(lsb_ctx* ctx, const SoftmaxArgs& a);
+lsb_status launch_expand(lsb_ctx* ctx, const ExpandArgs& a);
+
+// Bitmap helpers for the stage API.
+lsb_status launch_bitmap_from_dense(lsb_ctx* ctx, const int32_t* L, int B, uint32_t V, int t,
+                                    uint32_t* bitmap);
+lsb_status launch_bitmap_from_ids(lsb_ctx* ctx, const uint32_t* ids, uint32_t n,
+                                  uint32_t* bitmap);
+lsb_status launch_gather(lsb_ctx* ctx, const float* E, int d, const uint32_t* ids, uint32_t n,
+                         float* out);
+
+// Chooses the row-group size RB for a sentence of B rows (see k_step.cu).
+int choose_rb(int B);
+
+}  // namespace lsb

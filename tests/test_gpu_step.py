@@ -1,0 +1,154 @@
+"""Fused step parity: lsb_step over S sentences vs the oracle's restatement of
+decode()'s kLsh / kFull step body (src/beam_decoder.cpp:166-289), sentence by
+sentence, on identical seeded inputs. Codes, candidate lists, provenance and
+chosen (score, beam, word) triples are compared exactly in PARITY mode."""
+import numpy as np
+import pytest
+
+from oracle.oracle import oracle_full_step, oracle_step
+
+pytestmark = pytest.mark.gpu
+
+
+def make_world(o, V, d, K, u, W, seed=7, bias_strength=0.0):
+    E = o.gaussian(seed, V * d).reshape(V, d)
+    m = o.synth_model(V, d, seed, bias_strength, want=("bias",))
+    perm_seed, index_seed = o.mix_seed(seed, 1), o.mix_seed(seed, 2)
+    perms = o.generate_perms(d, u * W, K, perm_seed)
+    codes = o.hash_matrix(E, K, u, W, perms=perms)
+    bt = o.band_index_build(codes, index_seed)
+    return E, m["bias"], perms, bt, perm_seed, index_seed
+
+
+def make_state(o, S, B, d, seed, frozen_every=0, short=0):
+    hidden = o.gaussian(o.mix_seed(seed, 3), S * B * d).reshape(S, B, d)
+    rng = np.random.default_rng(seed)
+    scores = -rng.random((S, B)) * 4.0
+    finished = np.zeros((S, B), np.uint8)
+    n_hyp = np.full(S, B, np.int32)
+    if frozen_every:
+        finished[:, ::frozen_every] = 1
+        finished[:, 1] = 0
+    if short:
+        n_hyp[::2] = short
+    return hidden, scores, finished, n_hyp
+
+
+def run_gpu(ctx, E, bias, V, d, K, u, W, perm_seed, index_seed, S, B, T, t, specials, state,
+            mode=0, full=False):
+    from paper_1806_00588_b200 import Batch, Index, Model
+    m = Model(ctx, E, bias)
+    idx = None if full else Index(ctx, m, K=K, u=u, W=W, perm_seed=perm_seed,
+                                  index_seed=index_seed)
+    b = Batch(ctx, m, idx, S=S, B=B, T=T, t=t, specials=specials, mode=mode, full_vocab=full)
+    b.keep_probs(True)
+    hidden, scores, finished, n_hyp = state
+    res, hout = b.step_host(hidden, scores, finished, n_hyp, want_hidden=True)
+    return b, res, hout
+
+
+CASES = [
+    # V, d, K, u, W, S, B, T, t
+    (4000, 64, 8, 3, 16, 4, 12, 100, 2),
+    (4000, 64, 8, 3, 16, 3, 12, 0, 1),
+    (3000, 40, 4, 2, 20, 2, 5, 10, 3),
+    (2000, 64, 8, 3, 100, 2, 12, 0, 0),
+    (5000, 1003, 16, 3, 32, 2, 7, 50, 1),
+    (1500, 256, 16, 3, 300, 2, 12, 25, 5),
+]
+
+
+@pytest.mark.parametrize("V,d,K,u,W,S,B,T,t", CASES)
+@pytest.mark.parametrize("frozen", [False, True])
+def test_step_matches_oracle(ctx, oracle, V, d, K, u, W, S, B, T, t, frozen):
+    E, bias, perms, bt, ps, isd = make_world(oracle, V, d, K, u, W, seed=V + d,
+                                             bias_strength=8.0)
+    specials = [V - 1]
+    state = make_state(oracle, S, B, d, seed=V * 3 + d, frozen_every=3 if frozen else 0,
+                       short=(B // 2 if frozen else 0))
+    b, res, hout = run_gpu(ctx, E, bias, V, d, K, u, W, ps, isd, S, B, T, t, specials, state)
+    hidden, scores, finished, n_hyp = state
+    for s in range(S):
+        want = oracle_step(oracle, bt, perms, E, bias, K, u, W, hidden[s], scores[s],
+                           finished[s], int(n_hyp[s]), B, T, t, specials)
+        ids, prov = b.candidates(s)
+        np.testing.assert_array_equal(ids, want["ids"])
+        assert prov == want["prov"]
+        codes = b.query_codes(s, W)[want["live"]]
+        np.testing.assert_array_equal(codes, want["codes"])
+        probs = b.probs(s)
+        np.testing.assert_array_equal(probs.view(np.uint32), want["probs"].view(np.uint32))
+        ws, wb, ww = want["choices"]
+        assert len(res[s]) == len(ws)
+        got = np.array([c[2] for c in res[s]]), np.array([c[1] for c in res[s]])
+        np.testing.assert_array_equal(got[0], ww)
+        np.testing.assert_array_equal(got[1], wb)
+        np.testing.assert_array_equal(np.array([c[0] for c in res[s]]), ws)
+        for k, (_, beam, _) in enumerate(res[s]):  # hidden-state reorder
+            np.testing.assert_array_equal(hout[s, k], hidden[s, beam])
+
+
+def test_step_config1_shape(ctx, oracle):
+    """BASELINE config 1 shapes: V=40k, d=1000, B=12, K=8, u=3, W=16, T=1000, t=2."""
+    V, d, K, u, W, B, T, t, S = 40000, 1000, 8, 3, 16, 12, 1000, 2, 2
+    E, bias, perms, bt, ps, isd = make_world(oracle, V, d, K, u, W, seed=7)
+    state = make_state(oracle, S, B, d, seed=7)
+    b, res, _ = run_gpu(ctx, E, bias, V, d, K, u, W, ps, isd, S, B, T, t, [V - 1], state)
+    hidden, scores, finished, n_hyp = state
+    for s in range(S):
+        want = oracle_step(oracle, bt, perms, E, bias, K, u, W, hidden[s], scores[s],
+                           finished[s], B, B, T, t, [V - 1])
+        ids, prov = b.candidates(s)
+        np.testing.assert_array_equal(ids, want["ids"])
+        ws, wb, ww = want["choices"]
+        assert [c[2] for c in res[s]] == ww.tolist()
+        assert [c[1] for c in res[s]] == wb.tolist()
+        np.testing.assert_array_equal(np.array([c[0] for c in res[s]]), ws)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_full_vocab_step(ctx, oracle, mode):
+    V, d, S, B = 3000, 64, 3, 6
+    E = oracle.gaussian(11, V * d).reshape(V, d)
+    bias = oracle.synth_model(V, d, 11, 8.0, want=("bias",))["bias"]
+    state = make_state(oracle, S, B, d, seed=5, frozen_every=4)
+    b, res, _ = run_gpu(ctx, E, bias, V, d, 8, 3, 16, 1, 2, S, B, 0, 0, [V - 1], state,
+                        mode=mode, full=True)
+    hidden, scores, finished, n_hyp = state
+    for s in range(S):
+        want = oracle_full_step(oracle, E, bias, hidden[s], scores[s], finished[s], B, B)
+        ws, wb, ww = want["choices"]
+        assert [c[2] for c in res[s]] == ww.tolist()
+        assert [c[1] for c in res[s]] == wb.tolist()
+        if mode == 0:
+            np.testing.assert_array_equal(np.array([c[0] for c in res[s]]), ws)
+        else:
+            np.testing.assert_allclose(np.array([c[0] for c in res[s]]), ws, rtol=1e-5)
+
+
+def test_step_nan_hidden_rejected(ctx, oracle):
+    V, d, K, u, W, S, B = 500, 16, 4, 2, 8, 1, 2
+    E, bias, perms, bt, ps, isd = make_world(oracle, V, d, K, u, W)
+    hidden, scores, finished, n_hyp = make_state(oracle, S, B, d, seed=3)
+    hidden[0, 1, 3] = np.nan
+    with pytest.raises(ValueError):
+        run_gpu(ctx, E, bias, V, d, K, u, W, ps, isd, S, B, 10, 1, [V - 1],
+                (hidden, scores, finished, n_hyp))
+
+
+def test_batch_config_validation(ctx, oracle):
+    from paper_1806_00588_b200 import Batch, Index, Model
+    V, d = 300, 16
+    E = oracle.gaussian(1, V * d).reshape(V, d)
+    m = Model(ctx, E)
+    idx = Index(ctx, m, K=4, u=2, W=20, perm_seed=5, index_seed=6)
+    with pytest.raises(ValueError):
+        Batch(ctx, m, idx, S=1, B=0)
+    with pytest.raises(ValueError):
+        Batch(ctx, m, idx, S=1, B=4, T=301)
+    with pytest.raises(ValueError):
+        Batch(ctx, m, idx, S=1, B=4, t=21)
+    with pytest.raises(ValueError):
+        Batch(ctx, m, idx, S=1, B=4, specials=[300])
+    with pytest.raises(ValueError):
+        Batch(ctx, m, None, S=1, B=4)  # lsh mode requires an index
