@@ -1,0 +1,26 @@
+#!/bin/bash
+# One GPU-box pass: parity tests, smoke, bench, ncu launch list and one
+# `ncu --set full` capture of the named kernels. Outputs go to gpurun_out/.
+# usage: scripts/gpu_round.sh [tag] [kernel-regex ...]
+TAG=${1:-r01}
+shift || true
+KERNELS=${*:-k_logits k_probe_count}
+OUT=gpurun_out/$TAG
+mkdir -p "$OUT"
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > "$OUT/gpu.txt" 2>&1
+lscpu > "$OUT/lscpu.txt" 2>&1
+timeout 1200 python -m pytest tests -m gpu -x -q > "$OUT/pytest_gpu.log" 2>&1
+echo "pytest exit $?" >> "$OUT/pytest_gpu.log"
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1
+echo "smoke exit $?" >> "$OUT/smoke.log"
+timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"
+echo "bench exit $?" >> "$OUT/bench.err"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'^k_' -c 400 --csv \
+  --log-file "$OUT/launches.csv" python bench.py --steps 20 --warmup 3 --no-cpu-baseline \
+  --no-extras > "$OUT/ncu_launch_bench.log" 2>&1
+for k in $KERNELS; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^$k" -s 60 -c 1 \
+    -f -o "$OUT/prof_$k" python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-extras \
+    > "$OUT/ncu_full_$k.log" 2>&1
+done
+echo done > "$OUT/DONE"
