@@ -1,0 +1,317 @@
+// k_logits.cu -- K4: logits = H . E[ids]^T + bias[ids] over the candidate set.
+//
+// Replaces gather_embeddings + compute_logits + the bias loop of decode()
+// (src/candidate_selector.cpp:105-119, src/beam_decoder.cpp:23-44, :237-247).
+// E_LSH is never materialised: each CTA owns RB hypothesis rows x 128*CB
+// candidate columns and streams the candidates' embedding rows straight from
+// E (row gather by id) into shared memory with cp.async, d in chunks of 32
+// floats through a 3-stage ring, so the inner loop reads only shared memory:
+// the H row chunk as a warp-wide broadcast and each thread's own E row with
+// conflict-free 16-byte loads (row pitch 36 floats = 4 mod 32 banks).
+//
+// Jobs (one CTA each):
+//  * shared block: candidate positions [0, n_shared) are ids 0..T-1 for every
+//    sentence (the top-T prefix, src/candidate_selector.cpp:57-103), so they
+//    are scored once for all S*B rows in groups of RB rows;
+//  * survivors: per (sentence, row group), X CTAs stride over that
+//    sentence's remaining candidate positions [n_shared, n_cand[s]).
+//
+// PARITY keeps four lane accumulators per output and adds fl(h*e) with
+// separate FMUL/FADD in the reference's SSE order (lane j takes columns
+// c = j mod 4 ascending; the d mod 4 tail goes to lane 0; final
+// ((l0+l1)+l2)+l3), which GCC -O3 emits for the omp-simd reduction at
+// src/beam_decoder.cpp:34-42 -> bit-identical logits. FAST uses one FFMA
+// chain per output.
+#include <algorithm>
+
+#include "k_step.cuh"
+
+namespace lsb {
+
+constexpr int kLT = 128;        // threads per CTA
+constexpr int kKC = 32;         // floats of d per pipeline stage
+constexpr int kKS = kKC + 4;    // shared-memory row pitch in floats
+constexpr int kStages = 3;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(src),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(src),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int RB, int CB>
+constexpr size_t logits_smem_bytes() {
+  return static_cast<size_t>(kStages) * (kLT * CB + RB) * kKS * 4 + kLT * CB * 4;
+}
+
+template <int RB, int CB, bool PARITY, bool VEC>
+__global__ void __launch_bounds__(kLT) k_logits(LogitsArgs a) {
+  extern __shared__ __align__(16) float sm[];
+  constexpr int CT = kLT * CB;
+  constexpr int STAGE = (CT + RB) * kKS;
+  constexpr int NA = PARITY ? 4 : 1;
+  uint32_t* sid = reinterpret_cast<uint32_t*>(sm + kStages * STAGE);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int d = a.d;
+  const int d4 = d & ~3;
+  const int nchunks = (d + kKC - 1) / kKC;
+
+  const bool shared_job = static_cast<int>(blockIdx.x) < a.jobs_shared;
+  int row0, rowlim, tile_first, tile_step, s = 0;
+  uint32_t m = 0;
+  if (shared_job) {
+    const int rg = blockIdx.x / a.ctiles_shared;
+    row0 = rg * RB;
+    rowlim = a.R_total;
+    tile_first = blockIdx.x % a.ctiles_shared;
+    tile_step = a.ctiles_shared;  // exactly one tile
+    m = a.n_shared;
+  } else {
+    const int e = blockIdx.x - a.jobs_shared;
+    s = e / (a.G * a.X);
+    const int g = (e / a.X) % a.G;
+    row0 = s * a.Bsent + g * RB;
+    rowlim = s * a.Bsent + a.Bsent;
+    tile_first = e % a.X;
+    tile_step = a.X;
+    m = a.n_cand[s] > a.n_shared ? a.n_cand[s] - a.n_shared : 0u;
+  }
+  const uint32_t* list = shared_job ? nullptr : a.ids + static_cast<size_t>(s) * a.ncap + a.n_shared;
+
+  const int ntiles = static_cast<int>((m + CT - 1) / CT);
+  for (int tile = tile_first; tile < ntiles; tile += tile_step) {
+    const uint32_t t0 = static_cast<uint32_t>(tile) * CT;
+    const int ncols = static_cast<int>(min(static_cast<uint32_t>(CT), m - t0));
+    const uint32_t col0 = (shared_job ? 0u : a.n_shared) + t0;
+    __syncthreads();  // previous tile's readers are done with sid / stages
+    for (int c = tid; c < CT; c += kLT)
+      sid[c] = c < ncols ? (list ? __ldg(list + t0 + c) : t0 + c) : 0u;
+    __syncthreads();
+
+    auto load_chunk = [&](int stage, int kc) {
+      float* Es = sm + stage * STAGE;
+      float* Hs = Es + CT * kKS;
+      const int c0 = kc * kKC;
+      if constexpr (VEC) {
+#pragma unroll
+        for (int i = 0; i < 8 * CB; ++i) {
+          const int q = tid + kLT * i;
+          const int col = q >> 3, part = q & 7;
+          const int k = c0 + part * 4;
+          const bool ok = col < ncols && k < d;
+          const float* src = ok ? a.E + static_cast<size_t>(sid[col]) * d + k : a.E;
+          cp_async16(Es + col * kKS + part * 4, src, ok ? 16 : 0);
+        }
+        for (int q = tid; q < RB * 8; q += kLT) {
+          const int rb = q >> 3, part = q & 7;
+          const int k = c0 + part * 4;
+          const bool ok = row0 + rb < rowlim && k < d;
+          const float* src = ok ? a.H + static_cast<size_t>(row0 + rb) * d + k : a.H;
+          cp_async16(Hs + rb * kKS + part * 4, src, ok ? 16 : 0);
+        }
+      } else {
+        for (int q = tid; q < CT * kKC; q += kLT) {
+          const int col = q >> 5, kk = q & 31;
+          const bool ok = col < ncols && c0 + kk < d;
+          const float* src = ok ? a.E + static_cast<size_t>(sid[col]) * d + c0 + kk : a.E;
+          cp_async4(Es + col * kKS + kk, src, ok ? 4 : 0);
+        }
+        for (int q = tid; q < RB * kKC; q += kLT) {
+          const int rb = q >> 5, kk = q & 31;
+          const bool ok = row0 + rb < rowlim && c0 + kk < d;
+          const float* src = ok ? a.H + static_cast<size_t>(row0 + rb) * d + c0 + kk : a.H;
+          cp_async4(Hs + rb * kKS + kk, src, ok ? 4 : 0);
+        }
+      }
+    };
+
+    float acc[RB][CB][NA];
+#pragma unroll
+    for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+      for (int cb = 0; cb < CB; ++cb)
+#pragma unroll
+        for (int k = 0; k < NA; ++k) acc[rb][cb][k] = 0.0f;
+
+#pragma unroll
+    for (int st = 0; st < kStages - 1; ++st) {
+      if (st < nchunks) load_chunk(st, st);
+      cp_async_commit();
+    }
+    // a warp whose 32 columns are all past the tile end skips the math
+    const bool warp_live = warp * 32 < ncols;
+    for (int kc = 0; kc < nchunks; ++kc) {
+      cp_async_wait<kStages - 2>();
+      __syncthreads();
+      {
+        const int nk = kc + kStages - 1;
+        if (nk < nchunks) load_chunk(nk % kStages, nk);
+        cp_async_commit();
+      }
+      const float* Es = sm + (kc % kStages) * STAGE;
+      const float* Hs = Es + CT * kKS;
+      const int kv = max(0, min(kKC, d4 - kc * kKC)) >> 2;  // full 4-lane groups
+      if (warp_live) {
+#pragma unroll 4
+        for (int k4 = 0; k4 < kv; ++k4) {
+          float4 e[CB];
+#pragma unroll
+          for (int cb = 0; cb < CB; ++cb)
+            e[cb] = *reinterpret_cast<const float4*>(Es + (tid + cb * kLT) * kKS + k4 * 4);
+#pragma unroll
+          for (int rb = 0; rb < RB; ++rb) {
+            const float4 h = *reinterpret_cast<const float4*>(Hs + rb * kKS + k4 * 4);
+#pragma unroll
+            for (int cb = 0; cb < CB; ++cb) {
+              if constexpr (PARITY) {
+                acc[rb][cb][0] = __fadd_rn(acc[rb][cb][0], __fmul_rn(h.x, e[cb].x));
+                acc[rb][cb][1] = __fadd_rn(acc[rb][cb][1], __fmul_rn(h.y, e[cb].y));
+                acc[rb][cb][2] = __fadd_rn(acc[rb][cb][2], __fmul_rn(h.z, e[cb].z));
+                acc[rb][cb][3] = __fadd_rn(acc[rb][cb][3], __fmul_rn(h.w, e[cb].w));
+              } else {
+                float x = acc[rb][cb][0];
+                x = fmaf(h.x, e[cb].x, x);
+                x = fmaf(h.y, e[cb].y, x);
+                x = fmaf(h.z, e[cb].z, x);
+                x = fmaf(h.w, e[cb].w, x);
+                acc[rb][cb][0] = x;
+              }
+            }
+          }
+        }
+      }
+    }
+    cp_async_wait<0>();
+    // the d mod 4 tail (all of d when d < 4) sits in the last chunk: lane 0
+    if (d4 < d && warp_live) {
+      const int cl = (nchunks - 1) * kKC;
+      const float* Es = sm + ((nchunks - 1) % kStages) * STAGE;
+      const float* Hs = Es + CT * kKS;
+      for (int k = d4; k < d; ++k) {
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+          const float h = Hs[rb * kKS + k - cl];
+#pragma unroll
+          for (int cb = 0; cb < CB; ++cb) {
+            const float e = Es[(tid + cb * kLT) * kKS + k - cl];
+            if (PARITY) acc[rb][cb][0] = __fadd_rn(__fmul_rn(h, e), acc[rb][cb][0]);
+            else acc[rb][cb][0] = fmaf(h, e, acc[rb][cb][0]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int cb = 0; cb < CB; ++cb) {
+      const int c = tid + kLT * cb;
+      if (c >= ncols) continue;
+      const float bias = a.bias ? __ldg(a.bias + sid[c]) : 0.0f;
+      const size_t col = col0 + c;
+#pragma unroll
+      for (int rb = 0; rb < RB; ++rb) {
+        const int r = row0 + rb;
+        if (r >= rowlim) continue;
+        float v;
+        if constexpr (PARITY) {
+          v = __fadd_rn(0.0f, acc[rb][cb][0]);
+          v = __fadd_rn(v, acc[rb][cb][1]);
+          v = __fadd_rn(v, acc[rb][cb][2]);
+          v = __fadd_rn(v, acc[rb][cb][3]);
+        } else {
+          v = acc[rb][cb][0];
+        }
+        if (a.bias) v = __fadd_rn(v, bias);
+        a.out[static_cast<size_t>(r) * a.ldo + col] = v;
+      }
+    }
+  }
+}
+
+int choose_rb(int B) {
+  static const int opts[] = {16, 12, 10, 8, 6, 4, 2, 1};
+  int best = 1, best_cost = 1 << 30;
+  for (int rb : opts) {
+    if (rb > B && rb != 1) continue;
+    const int groups = (B + rb - 1) / rb;
+    const int pad = groups * rb - B;
+    // fewest groups first (fewest E-tile re-reads), then least padding
+    const int cost = groups * 64 + pad;
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = rb;
+    }
+  }
+  return best;
+}
+
+template <int RB, int CB, bool PARITY, bool VEC>
+static lsb_status launch_variant(lsb_ctx* ctx, const LogitsArgs& a, int grid) {
+  constexpr size_t smem = logits_smem_bytes<RB, CB>();
+  static bool configured = false;
+  if (!configured) {
+    LSB_CUDA(cudaFuncSetAttribute(k_logits<RB, CB, PARITY, VEC>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    configured = true;
+  }
+  k_logits<RB, CB, PARITY, VEC><<<grid, kLT, smem, ctx->stream>>>(a);
+  LSB_LAUNCHED(ctx, "k_logits");
+  return LSB_OK;
+}
+
+template <int RB, int CB, bool PARITY>
+static lsb_status launch_logits_rb(lsb_ctx* ctx, LogitsArgs a, int target) {
+  constexpr int CT = kLT * CB;
+  const int rgroups = (a.R_total + RB - 1) / RB;
+  a.ctiles_shared = static_cast<int>((a.n_shared + CT - 1) / CT);
+  a.jobs_shared = a.n_shared ? rgroups * a.ctiles_shared : 0;
+  a.G = (a.Bsent + RB - 1) / RB;
+  if (a.ids && a.S > 0) {
+    const size_t max_tiles = (a.ncap > a.n_shared ? a.ncap - a.n_shared : 0) / CT + 1;
+    const int want = std::max(1, (target - a.jobs_shared) / std::max(1, a.S * a.G));
+    a.X = static_cast<int>(std::min<size_t>({static_cast<size_t>(want), size_t(64), max_tiles}));
+  } else {
+    a.X = 0;
+  }
+  const int grid = a.jobs_shared + a.S * a.G * a.X;
+  if (grid == 0) return LSB_OK;
+  const bool vec = (a.d & 3) == 0 && (reinterpret_cast<uintptr_t>(a.E) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(a.H) & 15) == 0;
+  return vec ? launch_variant<RB, CB, PARITY, true>(ctx, a, grid)
+             : launch_variant<RB, CB, PARITY, false>(ctx, a, grid);
+}
+
+// PARITY: one column per thread (8 FP instructions per 16-byte E load keep
+// shared-memory wavefronts under the FMUL/FADD issue rate). FAST does half
+// the FP work per load, so it takes two columns per thread.
+lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_ctas) {
+  const bool fast = mode == LSB_MODE_FAST;
+#define LSB_RB(R)                                                        \
+  case R:                                                                \
+    return fast ? launch_logits_rb<R, 2, false>(ctx, a, target_ctas)     \
+                : launch_logits_rb<R, 1, true>(ctx, a, target_ctas);
+  switch (choose_rb(a.Bsent)) {
+    LSB_RB(16)
+    LSB_RB(12)
+    LSB_RB(10)
+    LSB_RB(8)
+    LSB_RB(6)
+    LSB_RB(4)
+    LSB_RB(2)
+    default:
+      return fast ? launch_logits_rb<1, 2, false>(ctx, a, target_ctas)
+                  : launch_logits_rb<1, 1, true>(ctx, a, target_ctas);
+  }
+#undef LSB_RB
+}
+
+}  // namespace lsb
