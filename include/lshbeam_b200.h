@@ -197,6 +197,7 @@ typedef struct lsb_step_config {
   int nspec;
   lsb_mode mode;
   int full_vocab;           /* 1 = kFull: score all of V, no LSH stages   */
+  int top_only;             /* 1 = kTopOnly: [0,T) U specials, no index   */
 } lsb_step_config;
 
 /* Validates like DecodeConfig::validate (src/candidate_selector.cpp:121-132). */
@@ -253,6 +254,77 @@ lsb_status lsb_batch_keep_probs(lsb_batch* b, int on);
 lsb_status lsb_batch_profile(lsb_batch* b, int on);
 lsb_status lsb_batch_stage_ms(lsb_batch* b, float* ms5);
 lsb_status lsb_batch_stage_totals(lsb_batch* b, float* ms5, int* nsteps);
+
+/* ------------------------------------------------ 6. device memory helpers
+ * So callers (the C++ drop-in layer, cgo/JNI bindings) never need their own
+ * CUDA runtime: allocations on the context's device and copies ordered on
+ * its stream. lsb_copy_to_host synchronises the stream and surfaces device
+ * errors like lsb_ctx_sync. */
+lsb_status lsb_device_alloc(lsb_ctx* ctx, size_t bytes, void** out);
+lsb_status lsb_device_free(lsb_ctx* ctx, void* p);
+lsb_status lsb_copy_to_device(lsb_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes);
+lsb_status lsb_copy_to_host(lsb_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes);
+
+/* ----------------------------------- 7. drop-in support (C++ layer, I/O)
+ * Entry points the C++ drop-in API (include/lshbeam/*.hpp) needs besides the
+ * per-step path. */
+
+/* Cuckoo slot placement for index builds on this context. 0 (default):
+ * REFERENCE placement -- per band the entries are inserted in the reference's
+ * order with its swap-and-flip eviction chain, so slots, multipliers and
+ * rebuild counts equal CuckooTable::build's (src/band_index.cpp:32-71;
+ * deterministic, WTAIDX1 bytes match). 1: PARALLEL placement -- one thread
+ * per entry with 64-bit atomicExch eviction chains (same lookups, different
+ * slot order). */
+lsb_status lsb_ctx_set_parallel_cuckoo(lsb_ctx* ctx, int on);
+/* log2 of the per-array capacity for n entries: max(1, ceil(log2 n))
+ * (src/band_index.cpp:39). */
+uint32_t lsb_cuckoo_log2_capacity(size_t n_entries);
+/* CuckooTable::build(entries, seed) (src/band_index.cpp:32-71) on the device:
+ * n distinct keys with their spans -> lg, the two multipliers and
+ * 2*2^lg slots as (key, start, length) triples (kEmptyCode = empty).
+ * LSB_EINVAL for a sentinel key, LSB_ERUNTIME when the rebuild budget runs out. */
+lsb_status lsb_cuckoo_build(lsb_ctx* ctx, const uint32_t* keys, const uint32_t* starts,
+                            const uint32_t* lens, uint32_t n, uint64_t seed, uint32_t* lg_out,
+                            uint64_t* mul2_out, uint32_t* slots_out, uint32_t* attempts_out);
+/* wta_hash_vector over n rows (src/wta_hash.cpp:75-92, :119-125): the
+ * P = num_perms raw argmax indices per row, unpacked (K >= 1). */
+lsb_status lsb_wta_indices(lsb_ctx* ctx, const float* M_host, int64_t n, int d,
+                           const uint32_t* perms_host, int P, int K, uint32_t* idx_host);
+/* Uploads a host-described index: the raw-state constructors
+ * CuckooTable(lg, mul0, mul1, slots) / BandIndex(vocab, W, word_ids, tables)
+ * (include/lshbeam/band_index.hpp) and load_lsh_index (src/band_index.cpp:245-289).
+ * word_ids_host: W x vocab (may be NULL: spans then index zeros); lg_host[W];
+ * mul_host[2W]; slots_host: per band 2*2^lg (key,start,length) triples,
+ * bands back to back. perms_host (u*W x K, may be NULL) attaches the WTA
+ * permutations so the index can serve lsb_step. */
+lsb_status lsb_index_import(lsb_ctx* ctx, uint32_t vocab, int W, const uint32_t* word_ids_host,
+                            const uint32_t* lg_host, const uint64_t* mul_host,
+                            const uint32_t* slots_host, const uint32_t* perms_host, int K, int u,
+                            int dim, uint64_t perm_seed, lsb_index** out);
+
+/* The recurrence of the synthetic scorer, h' = tanh(W_h h + W_e E[token])
+ * (src/model_provider.cpp:83-102), on the device: FP32 in the reference's
+ * 4-lane order without FMA, tanh evaluated in double and rounded. */
+typedef struct lsb_recurrent lsb_recurrent;  /* device W_h, W_e (d x d)  */
+lsb_status lsb_recurrent_create(lsb_ctx* ctx, const float* wh_host, const float* we_host, int d,
+                                lsb_recurrent** out);
+lsb_status lsb_recurrent_destroy(lsb_recurrent* r);
+/* n hypotheses, device buffers: tokens[k] < 0 copies hidden_in[k] (a frozen
+ * hypothesis is carried unchanged). Asynchronous. */
+lsb_status lsb_recurrence(lsb_ctx* ctx, const lsb_model* model, const lsb_recurrent* rec,
+                          const float* hidden_in_dev, const int64_t* tokens_dev, int n,
+                          float* hidden_out_dev);
+/* step_hidden(model, h, token) with host vectors (synchronous). */
+lsb_status lsb_step_hidden(lsb_ctx* ctx, const lsb_model* model, const lsb_recurrent* rec,
+                           const float* h_host, uint32_t token, float* out_host);
+
+/* exact_topb_logits(H . E^T (+ bias), b) (src/eval_oracle.cpp:11-44): per row
+ * the b largest full-vocabulary logits, ties to the smaller id; rows x b ids
+ * and values to host buffers. H is a device pointer when H_on_device. */
+lsb_status lsb_exact_topb(lsb_ctx* ctx, const lsb_model* model, const float* H, int rows,
+                          int H_on_device, int b, int add_bias, uint32_t* ids_host,
+                          float* values_host);
 
 #ifdef __cplusplus
 }

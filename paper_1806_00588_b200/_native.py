@@ -30,7 +30,8 @@ class lsb_index_info(C.Structure):
 class lsb_step_config(C.Structure):
     _fields_ = [("S", C.c_int), ("B", C.c_int), ("top_merge", C.c_uint32),
                 ("threshold", C.c_int), ("specials", C.POINTER(C.c_uint32)),
-                ("nspec", C.c_int), ("mode", C.c_int), ("full_vocab", C.c_int)]
+                ("nspec", C.c_int), ("mode", C.c_int), ("full_vocab", C.c_int),
+                ("top_only", C.c_int)]
 
 
 class lsb_state_dev(C.Structure):

@@ -1,4 +1,12 @@
-"""Builds the in-tree CUDA library paper_1806_00588_b200/liblshbeam_b200.so.
+"""Builds the in-tree libraries:
+
+* paper_1806_00588_b200/liblshbeam_b200.so -- the CUDA kernels + C ABI
+  (include/lshbeam_b200.h);
+* paper_1806_00588_b200/liblshbeam.so -- the C++ drop-in API
+  (include/lshbeam/*.hpp, namespace lshbeam) over that C ABI, so C++ callers
+  of the reference library (its CLI, bench and test suites) link against the
+  GPU build unchanged.
+
 
 Explicit nvcc for sm_100a only (no PTX fallback, no other arch): every .cu
 under csrc/ is compiled to an object with -lineinfo (ncu source view) and
@@ -18,6 +26,10 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "liblshbeam_b200.so")
+CPP = os.path.join(PKG, "cpp")
+CPPLIB = os.path.join(PKG, "liblshbeam.so")
+CXX = os.environ.get("CXX_DROPIN", "/usr/bin/g++")
+CXXFLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-I" + os.path.join(ROOT, "include")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
@@ -58,9 +70,28 @@ def build(verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+    build_cpp()
     if verbose:
         print(LIB)
+        print(CPPLIB)
     return LIB
+
+
+def build_cpp() -> str:
+    """The C++ drop-in layer: g++ (C++20, like the reference) over cpp/*.cpp,
+    linked against liblshbeam_b200.so with an $ORIGIN rpath."""
+    srcs = sorted(glob.glob(os.path.join(CPP, "*.cpp")))
+    deps = srcs + sorted(glob.glob(os.path.join(CPP, "*.hpp"))) + sorted(
+        glob.glob(os.path.join(ROOT, "include", "lshbeam", "*.hpp"))) + [
+        os.path.join(ROOT, "include", "lshbeam_b200.h"), LIB, __file__]
+    if _newer(CPPLIB, deps):
+        return CPPLIB
+    cmd = [CXX, *CXXFLAGS, "-shared", "-o", CPPLIB, *srcs, "-L" + PKG, "-llshbeam_b200",
+           "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"C++ drop-in build failed:\n{r.stderr}")
+    return CPPLIB
 
 
 if __name__ == "__main__":

@@ -92,7 +92,7 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
   if (cfg->B > 64) return set_error("config: beam above 64 is not supported by the fused step"), LSB_EINVAL;
   if (cfg->S < 1) return set_error("config: at least one sentence"), LSB_EINVAL;
   if (cfg->top_merge > V) return set_error("config: T exceeds vocabulary size"), LSB_EINVAL;
-  if (!cfg->full_vocab) {
+  if (!cfg->full_vocab && !cfg->top_only) {
     if (!idx || !idx->has_perms)
       return set_error("decode: lsh mode requires an index"), LSB_EINVAL;
     if (idx->V != V || idx->dim != model->d)
@@ -110,7 +110,7 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
   auto* b = new lsb_batch;
   b->ctx = ctx;
   b->model = model;
-  b->idx = cfg->full_vocab ? nullptr : idx;
+  b->idx = (cfg->full_vocab || cfg->top_only) ? nullptr : idx;
   b->S = cfg->S;
   b->B = cfg->B;
   b->d = model->d;
@@ -217,8 +217,8 @@ lsb_status lsb_step(lsb_batch* b, const lsb_state_dev* in, const lsb_out_dev* ou
     b->ring_used = std::min(b->ring_used + 1, kRing);
     LSB_CUDA(cudaEventRecord(b->ev[0], st));
   }
-  // K1 + K2
-  if (b->cmode != 2) {
+  // K1 + K2 (kTopOnly has no index: the bitmap stays empty)
+  if (b->cmode != 2 && b->idx) {
     ProbeArgs pa{};
     pa.ix = b->idx->view();
     pa.hidden = in->hidden;

@@ -10,10 +10,14 @@
 //     on the code bits only (ids enter in ascending order, so the result is
 //     the reference's sort of (code<<32 | id), src/band_index.cpp:103-108),
 //     then the span table (code -> start, length).
-//     k_cuckoo_build  : one CTA per band, one thread per entry, 64-bit
-//     atomicExch eviction chains <= kMaxDisplacements hops; on any failure the
-//     band retries with the next multiplier pair of the reference's
-//     SplitMix64(mix_seed(seed, w)) schedule (src/band_index.cpp:44-70).
+//     k_cuckoo_build  : one CTA per band. REFERENCE placement (default): one
+//     thread inserts the band's entries in the reference's order with its
+//     swap-and-flip eviction chain, so slots, multipliers and rebuild count
+//     are identical to CuckooTable::build (deterministic; WTAIDX1 bytes
+//     match). PARALLEL placement: one thread per entry, 64-bit atomicExch
+//     eviction chains (lookups are placement-independent). Both cap chains at
+//     kMaxDisplacements hops and, on failure, retry with the next multiplier
+//     pair of SplitMix64(mix_seed(seed, w)) (src/band_index.cpp:44-70).
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -229,7 +233,7 @@ __global__ void __launch_bounds__(1024) k_cuckoo_build(
     const uint32_t* __restrict__ elen, const uint32_t* __restrict__ n_entries, uint32_t V,
     unsigned long long index_seed, BandMeta* __restrict__ bands,
     unsigned long long* __restrict__ tmp, uint4* __restrict__ slots,
-    uint32_t* __restrict__ attempts_out, uint32_t* err) {
+    uint32_t* __restrict__ attempts_out, uint32_t* err, int sequential) {
   __shared__ unsigned long long mul[2];
   __shared__ int fail;
   const int w = blockIdx.x;
@@ -248,7 +252,9 @@ __global__ void __launch_bounds__(1024) k_cuckoo_build(
     for (uint32_t s = threadIdx.x; s < 2 * cap; s += blockDim.x) t[s] = kEmpty64;
     __syncthreads();
     const unsigned long long m0 = mul[0], m1 = mul[1];
-    for (uint32_t e = threadIdx.x; e < ne; e += blockDim.x) {
+    const uint32_t e0 = sequential ? (threadIdx.x == 0 ? 0u : ne) : threadIdx.x;
+    const uint32_t estep = sequential ? 1u : blockDim.x;
+    for (uint32_t e = e0; e < ne; e += estep) {
       unsigned long long cur = (static_cast<unsigned long long>(ekey[off + e]) << 32) | e;
       int table = 0;
       bool placed = false;
@@ -262,7 +268,10 @@ __global__ void __launch_bounds__(1024) k_cuckoo_build(
         }
         table = 1 - table;  // the evictee moves to its other table
       }
-      if (!placed) fail = 1;
+      if (!placed) {
+        fail = 1;
+        if (sequential) break;  // the reference abandons the attempt here
+      }
     }
     __syncthreads();
     if (!fail) {
@@ -449,11 +458,31 @@ static lsb_status build_bands(lsb_ctx* ctx, lsb_index* idx, const uint32_t* code
                            cudaMemcpyHostToDevice, ctx->stream));
   k_cuckoo_build<<<W, 1024, 0, ctx->stream>>>(ekey.p, estart.p, elen.p, nent.p, V,
                                               idx->index_seed, idx->bands, tmp.p, idx->slots,
-                                              attempts.p, ctx->err_dev);
+                                              attempts.p, ctx->err_dev,
+                                              ctx->cuckoo_parallel ? 0 : 1);
   LSB_LAUNCHED(ctx, "k_cuckoo_build");
   LSB_CUDA(cudaMemcpyAsync(idx->bands_host.data(), idx->bands, W * sizeof(BandMeta),
                            cudaMemcpyDeviceToHost, ctx->stream));
   LSB_CUDA(cudaMemcpyAsync(&idx->attempts, attempts.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  return lsb_ctx_sync(ctx);
+}
+
+// One standalone table (CuckooTable::build): entries already on the device.
+lsb_status build_cuckoo_band(lsb_ctx* ctx, const uint32_t* keys, const uint32_t* starts,
+                             const uint32_t* lens, uint32_t n, uint64_t seed, uint32_t lg,
+                             uint4* slots_dev, BandMeta* meta_dev, uint32_t* attempts_dev) {
+  DevBuf<unsigned long long> tmp;
+  DevBuf<uint32_t> ne;
+  LSB_CUDA(tmp.alloc(2u << lg));
+  LSB_CUDA(ne.alloc(1));
+  const BandMeta m{1ull, 1ull, lg, 0};
+  LSB_CUDA(cudaMemcpyAsync(ne.p, &n, 4, cudaMemcpyHostToDevice, ctx->stream));
+  LSB_CUDA(cudaMemcpyAsync(meta_dev, &m, sizeof(m), cudaMemcpyHostToDevice, ctx->stream));
+  LSB_CUDA(cudaMemsetAsync(attempts_dev, 0, 4, ctx->stream));
+  k_cuckoo_build<<<1, 1024, 0, ctx->stream>>>(keys, starts, lens, ne.p, n, seed, meta_dev, tmp.p,
+                                             slots_dev, attempts_dev, ctx->err_dev,
+                                             ctx->cuckoo_parallel ? 0 : 1);
+  LSB_LAUNCHED(ctx, "k_cuckoo_build");
   return lsb_ctx_sync(ctx);
 }
 

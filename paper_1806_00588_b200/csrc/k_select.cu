@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kSelT) k_softmax_topb(SoftmaxArgs a) {
   TopEntry* out = a.top + static_cast<size_t>(row) * B;
   int head = 0;
   for (int k = 0; k < keep; ++k) {
-    float bp = head < cnt ? lp[head * kSelT + tid] : -1.0f;
+    float bp = head < cnt ? lp[head * kSelT + tid] : -INFINITY;
     uint32_t br = head < cnt ? lr[head * kSelT + tid] : 0xFFFFFFFFu;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {

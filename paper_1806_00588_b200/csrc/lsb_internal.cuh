@@ -58,6 +58,7 @@ struct lsb_ctx {
   uint32_t* err_dev = nullptr;   // device error word
   uint32_t* err_host = nullptr;  // pinned mirror
   uint64_t launches = 0;
+  int cuckoo_parallel = 0;        // 0: reference slot placement
 };
 
 struct lsb_model {

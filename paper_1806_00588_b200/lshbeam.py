@@ -291,12 +291,13 @@ class Batch:
 
     def __init__(self, ctx: Context, model: Model, index: Index | None, S: int, B: int,
                  T: int = 0, t: int = 1, specials=(), mode: int = PARITY,
-                 full_vocab: bool = False):
+                 full_vocab: bool = False, top_only: bool = False):
         self.ctx, self.lib = ctx, ctx.lib
         sp = _u32(list(specials)) if len(specials) else np.zeros(1, np.uint32)
         self._sp = sp
         cfg = N.lsb_step_config(S, B, T, t, sp.ctypes.data_as(C.POINTER(C.c_uint32)),
-                                len(specials), mode, 1 if full_vocab else 0)
+                                len(specials), mode, 1 if full_vocab else 0,
+                                1 if top_only else 0)
         h = C.c_void_p()
         N.check(self.lib.lsb_batch_create(ctx.h, model.h, index.h if index else None,
                                           C.byref(cfg), C.byref(h)), "lsb_batch_create")

@@ -1,0 +1,32 @@
+"""The reference's OWN unit suites (/root/reference/proj/tests/test_*.cpp,
+98 doctest cases) compiled unchanged against the C++ drop-in headers
+(include/lshbeam/*.hpp) and linked with liblshbeam.so -> liblshbeam_b200.so,
+so every hot-path call they make runs on the GPU. Built by
+tests/refsuite/Makefile from /root/reference at build() time; the binaries
+travel to the GPU box (git-ignored, not gpurun-ignored)."""
+import os
+import subprocess
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+BUILD = os.path.join(HERE, "refsuite", "_build")
+SUITES = ["test_wta_hash", "test_band_index", "test_candidate_selector", "test_model_provider",
+          "test_eval_oracle", "test_beam_decoder", "test_parallel_equivalence"]
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("suite", SUITES)
+def test_reference_suite_on_gpu(suite):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    exe = os.path.join(BUILD, suite)
+    if not os.path.exists(exe):
+        pytest.skip("tests/refsuite not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600,
+                       cwd=os.path.dirname(exe))
+    tail = "\n".join((r.stdout + r.stderr).splitlines()[-40:])
+    assert r.returncode == 0, tail
+    assert "| 0 failed" in r.stdout, tail
