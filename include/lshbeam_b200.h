@@ -326,6 +326,28 @@ lsb_status lsb_exact_topb(lsb_ctx* ctx, const lsb_model* model, const float* H, 
                           int H_on_device, int b, int add_bias, uint32_t* ids_host,
                           float* values_host);
 
+/* ---------------------------------- 8. vocabulary-sharded step (cfg 4)
+ * One rank's share of a decode step when E is split by contiguous vocabulary
+ * slices across ranks (the reference has no multi-device path; SURVEY
+ * §8(e)). The rank's lsb_batch is built over its slice (lsb_model of
+ * E[v0:v0+n], an index over the slice with the global permutation seed,
+ * T_local = clamp(T - v0, 0, n), specials shifted by -v0). Between the phases
+ * the caller all-gathers, in rank order, the S*B row maxima (float) and then
+ * the S*B row sums (double) and the S*B x lsb_shard_width() top entries.
+ * Every rank ends with identical choices and hidden_out; results equal the
+ * unsharded step (PARITY: bit-exact unless > 4 entries of one rank tie in p
+ * with the B-th winner). */
+typedef struct lsb_shard_top {
+  float e;        /* float(exp(l - global max)); < 0 marks an empty entry */
+  uint32_t word;  /* global word id */
+} lsb_shard_top;
+int lsb_shard_width(const lsb_batch* b); /* B' = B + 4 entries per row */
+lsb_status lsb_shard_phase1(lsb_batch* b, const lsb_state_dev* in, float* rowmax_dev);
+lsb_status lsb_shard_phase2(lsb_batch* b, const lsb_state_dev* in, const float* allmax_dev, int G,
+                            uint32_t word_base, double* rowsum_dev, lsb_shard_top* top_dev);
+lsb_status lsb_shard_phase3(lsb_batch* b, const lsb_state_dev* in, const double* allsum_dev,
+                            const lsb_shard_top* alltop_dev, int G, const lsb_out_dev* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -46,6 +46,10 @@ class lsb_out_dev(C.Structure):
 
 lsb_state_host = lsb_state_dev  # same layout, host pointers
 
+
+class lsb_shard_top(C.Structure):
+    _fields_ = [("e", C.c_float), ("word", C.c_uint32)]
+
 VP = C.c_void_p
 PP = C.POINTER(C.c_void_p)
 U32 = C.c_uint32
@@ -100,6 +104,30 @@ _SIGS = [
     ("lsb_batch_profile", C.c_int, [VP, C.c_int]),
     ("lsb_batch_stage_ms", C.c_int, [VP, VP]),
     ("lsb_batch_stage_totals", C.c_int, [VP, VP, C.POINTER(C.c_int)]),
+    # device memory helpers
+    ("lsb_device_alloc", C.c_int, [VP, C.c_size_t, PP]),
+    ("lsb_device_free", C.c_int, [VP, VP]),
+    ("lsb_copy_to_device", C.c_int, [VP, VP, VP, C.c_size_t]),
+    ("lsb_copy_to_host", C.c_int, [VP, VP, VP, C.c_size_t]),
+    # drop-in support
+    ("lsb_ctx_set_parallel_cuckoo", C.c_int, [VP, C.c_int]),
+    ("lsb_cuckoo_log2_capacity", U32, [C.c_size_t]),
+    ("lsb_cuckoo_build", C.c_int, [VP, VP, VP, VP, U32, U64, C.POINTER(U32), VP, VP,
+                                   C.POINTER(U32)]),
+    ("lsb_wta_indices", C.c_int, [VP, VP, I64, C.c_int, VP, C.c_int, C.c_int, VP]),
+    ("lsb_index_import", C.c_int, [VP, U32, C.c_int, VP, VP, VP, VP, VP, C.c_int, C.c_int,
+                                   C.c_int, U64, PP]),
+    ("lsb_recurrent_create", C.c_int, [VP, VP, VP, C.c_int, PP]),
+    ("lsb_recurrent_destroy", C.c_int, [VP]),
+    ("lsb_recurrence", C.c_int, [VP, VP, VP, VP, VP, C.c_int, VP]),
+    ("lsb_step_hidden", C.c_int, [VP, VP, VP, VP, U32, VP]),
+    ("lsb_exact_topb", C.c_int, [VP, VP, VP, C.c_int, C.c_int, C.c_int, C.c_int, VP, VP]),
+    # vocabulary-sharded step
+    ("lsb_shard_width", C.c_int, [VP]),
+    ("lsb_shard_phase1", C.c_int, [VP, C.POINTER(lsb_state_dev), VP]),
+    ("lsb_shard_phase2", C.c_int, [VP, C.POINTER(lsb_state_dev), VP, C.c_int, U32, VP, VP]),
+    ("lsb_shard_phase3", C.c_int, [VP, C.POINTER(lsb_state_dev), VP, VP, C.c_int,
+                                   C.POINTER(lsb_out_dev)]),
 ]
 
 EXPORTED = [s[0] for s in _SIGS]

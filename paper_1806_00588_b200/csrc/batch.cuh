@@ -1,0 +1,59 @@
+// batch.cuh -- host state of one lsb_batch (per-step scratch for S
+// sentences), shared by the fused step (capi_step.cu) and the vocabulary-
+// sharded step (capi_shard.cu).
+#pragma once
+
+#include <vector>
+
+#include "k_step.cuh"
+
+struct lsb_batch {
+  lsb_ctx* ctx = nullptr;
+  const lsb_model* model = nullptr;
+  const lsb_index* idx = nullptr;
+  int S = 0, B = 0, d = 0, t = 0;
+  uint32_t V = 0, T = 0;
+  lsb_mode mode = LSB_MODE_PARITY;
+  int cmode = 0;  // 0 threshold, 1 all words (t == 0), 2 full vocabulary
+  uint32_t n_shared = 0;
+  size_t ncap = 0;
+  uint32_t nwords = 0, slice_len = 0;
+  int counter_bytes = 1;
+  int nspec = 0;
+  int keep_probs = 0;
+  // device scratch
+  uint32_t* specials = nullptr;
+  uint32_t* qcodes = nullptr;
+  uint32_t* bitmap = nullptr;
+  uint32_t* ids = nullptr;
+  uint32_t* n_cand = nullptr;
+  uint32_t* prov = nullptr;
+  float* logits = nullptr;
+  lsb::TopEntry* top = nullptr;
+  int32_t* top_n = nullptr;
+  lsb::TopEntry* sh_top = nullptr;   // vocabulary-sharded step: local top-B'
+  int32_t* sh_topn = nullptr;
+  // staging for lsb_step_host
+  float* h_hidden = nullptr;
+  double* h_scores = nullptr;
+  uint8_t* h_finished = nullptr;
+  int32_t* h_nhyp = nullptr;
+  lsb_choice* h_choices = nullptr;
+  int32_t* h_nchoices = nullptr;
+  float* h_hidden_out = nullptr;
+  // last step (for the per-sentence views)
+  lsb_state_dev last{};
+  bool has_last = false;
+  // profiling: one set of 6 events per step in a ring, summed on demand
+  bool profile = false;
+  std::vector<cudaEvent_t> ring;  // kRing * 6
+  int ring_next = 0, ring_used = 0;
+  cudaEvent_t* ev = nullptr;       // current step's 6 events
+};
+
+
+namespace lsb {
+// K1+K2 -> K3 -> K4 of one step (profiling events 0..3): candidate sets in
+// b->ids / b->n_cand, logits in b->logits.
+lsb_status step_front(lsb_batch* b, const lsb_state_dev* in, int empty_is_error);
+}  // namespace lsb

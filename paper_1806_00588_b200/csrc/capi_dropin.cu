@@ -370,7 +370,7 @@ lsb_status lsb_recurrence(lsb_ctx* ctx, const lsb_model* model, const lsb_recurr
   const size_t smem = static_cast<size_t>(d) * 8;
   if (smem > ctx->smem_optin) return set_error("lsb_recurrence: dimension too large"), LSB_EINVAL;
   static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
+  if (smem > configured) {
     LSB_CUDA(cudaFuncSetAttribute(k_recurrence, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     configured = smem;

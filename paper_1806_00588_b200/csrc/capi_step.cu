@@ -9,51 +9,9 @@
 #include <cstring>
 #include <vector>
 
-#include "k_step.cuh"
+#include "batch.cuh"
 
 using namespace lsb;
-
-struct lsb_batch {
-  lsb_ctx* ctx = nullptr;
-  const lsb_model* model = nullptr;
-  const lsb_index* idx = nullptr;
-  int S = 0, B = 0, d = 0, t = 0;
-  uint32_t V = 0, T = 0;
-  lsb_mode mode = LSB_MODE_PARITY;
-  int cmode = 0;  // 0 threshold, 1 all words (t == 0), 2 full vocabulary
-  uint32_t n_shared = 0;
-  size_t ncap = 0;
-  uint32_t nwords = 0, slice_len = 0;
-  int counter_bytes = 1;
-  int nspec = 0;
-  int keep_probs = 0;
-  // device scratch
-  uint32_t* specials = nullptr;
-  uint32_t* qcodes = nullptr;
-  uint32_t* bitmap = nullptr;
-  uint32_t* ids = nullptr;
-  uint32_t* n_cand = nullptr;
-  uint32_t* prov = nullptr;
-  float* logits = nullptr;
-  TopEntry* top = nullptr;
-  int32_t* top_n = nullptr;
-  // staging for lsb_step_host
-  float* h_hidden = nullptr;
-  double* h_scores = nullptr;
-  uint8_t* h_finished = nullptr;
-  int32_t* h_nhyp = nullptr;
-  lsb_choice* h_choices = nullptr;
-  int32_t* h_nchoices = nullptr;
-  float* h_hidden_out = nullptr;
-  // last step (for the per-sentence views)
-  lsb_state_dev last{};
-  bool has_last = false;
-  // profiling: one set of 6 events per step in a ring, summed on demand
-  bool profile = false;
-  std::vector<cudaEvent_t> ring;  // kRing * 6
-  int ring_next = 0, ring_used = 0;
-  cudaEvent_t* ev = nullptr;       // current step's 6 events
-};
 
 static constexpr int kRing = 1024;
 
@@ -69,7 +27,7 @@ lsb_status free_batch(lsb_batch* b) {
   void* ptrs[] = {b->specials, b->qcodes,   b->bitmap,     b->ids,          b->n_cand,
                   b->prov,     b->logits,   b->top,        b->top_n,        b->h_hidden,
                   b->h_scores, b->h_finished, b->h_nhyp,   b->h_choices,    b->h_nchoices,
-                  b->h_hidden_out};
+                  b->h_hidden_out, b->sh_top, b->sh_topn};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : b->ring)
@@ -79,6 +37,77 @@ lsb_status free_batch(lsb_batch* b) {
 }
 
 }  // namespace
+
+lsb_status lsb::step_front(lsb_batch* b, const lsb_state_dev* in, int empty_is_error) {
+  lsb_ctx* ctx = b->ctx;
+  cudaStream_t st = ctx->stream;
+  const int R = b->S * b->B;
+  lsb_status rc;
+  if (b->profile) {
+    b->ev = &b->ring[static_cast<size_t>(b->ring_next) * 6];
+    b->ring_next = (b->ring_next + 1) % kRing;
+    b->ring_used = std::min(b->ring_used + 1, kRing);
+    LSB_CUDA(cudaEventRecord(b->ev[0], st));
+  }
+  // K1 + K2 (kTopOnly has no index: the bitmap stays empty)
+  if (b->cmode != 2 && b->idx) {
+    ProbeArgs pa{};
+    pa.ix = b->idx->view();
+    pa.hidden = in->hidden;
+    pa.finished = in->finished;
+    pa.n_hyp = in->n_hyp;
+    pa.S = b->S;
+    pa.B = b->B;
+    pa.t = b->t;
+    pa.slice_len = b->slice_len;
+    pa.counter_bytes = b->counter_bytes;
+    pa.qcodes = b->qcodes;
+    pa.bitmap = b->bitmap;
+    pa.nwords = b->nwords;
+    pa.err = ctx->err_dev;
+    if ((rc = launch_probe(ctx, pa))) return rc;
+  }
+  if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[1], st));
+  // K3
+  CompactArgs ca{};
+  ca.bitmap_in = b->bitmap;
+  ca.bitmap_clear = b->bitmap;
+  ca.nwords = b->nwords;
+  ca.V = b->V;
+  ca.T = b->T;
+  ca.mode = b->cmode;
+  ca.specials = b->specials;
+  ca.nspec = b->nspec;
+  ca.ids = b->ids;
+  ca.ncap = b->ncap;
+  ca.n_cand = b->n_cand;
+  ca.prov = b->prov;
+  ca.empty_is_error = empty_is_error;
+  ca.n_hyp = in->n_hyp;
+  ca.finished = in->finished;
+  ca.B = b->B;
+  ca.err = ctx->err_dev;
+  if ((rc = launch_compact(ctx, ca, b->S))) return rc;
+  if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[2], st));
+  // K4
+  LogitsArgs la{};
+  la.H = in->hidden;
+  la.d = b->d;
+  la.R_total = R;
+  la.Bsent = b->B;
+  la.E = b->model->E;
+  la.bias = b->model->bias;
+  la.n_shared = b->n_shared;
+  la.ids = b->cmode == 0 ? b->ids : nullptr;
+  la.ncap = b->ncap;
+  la.n_cand = b->n_cand;
+  la.S = b->S;
+  la.out = b->logits;
+  la.ldo = b->ncap;
+  if ((rc = launch_logits(ctx, la, b->mode, ctx->sm_count * 8))) return rc;
+  if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[3], st));
+  return LSB_OK;
+}
 
 extern "C" {
 
@@ -210,70 +239,8 @@ lsb_status lsb_step(lsb_batch* b, const lsb_state_dev* in, const lsb_out_dev* ou
   lsb_ctx* ctx = b->ctx;
   cudaStream_t st = ctx->stream;
   const int R = b->S * b->B;
-  lsb_status rc;
-  if (b->profile) {
-    b->ev = &b->ring[static_cast<size_t>(b->ring_next) * 6];
-    b->ring_next = (b->ring_next + 1) % kRing;
-    b->ring_used = std::min(b->ring_used + 1, kRing);
-    LSB_CUDA(cudaEventRecord(b->ev[0], st));
-  }
-  // K1 + K2 (kTopOnly has no index: the bitmap stays empty)
-  if (b->cmode != 2 && b->idx) {
-    ProbeArgs pa{};
-    pa.ix = b->idx->view();
-    pa.hidden = in->hidden;
-    pa.finished = in->finished;
-    pa.n_hyp = in->n_hyp;
-    pa.S = b->S;
-    pa.B = b->B;
-    pa.t = b->t;
-    pa.slice_len = b->slice_len;
-    pa.counter_bytes = b->counter_bytes;
-    pa.qcodes = b->qcodes;
-    pa.bitmap = b->bitmap;
-    pa.nwords = b->nwords;
-    pa.err = ctx->err_dev;
-    if ((rc = launch_probe(ctx, pa))) return rc;
-  }
-  if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[1], st));
-  // K3
-  CompactArgs ca{};
-  ca.bitmap_in = b->bitmap;
-  ca.bitmap_clear = b->bitmap;
-  ca.nwords = b->nwords;
-  ca.V = b->V;
-  ca.T = b->T;
-  ca.mode = b->cmode;
-  ca.specials = b->specials;
-  ca.nspec = b->nspec;
-  ca.ids = b->ids;
-  ca.ncap = b->ncap;
-  ca.n_cand = b->n_cand;
-  ca.prov = b->prov;
-  ca.empty_is_error = 1;
-  ca.n_hyp = in->n_hyp;
-  ca.finished = in->finished;
-  ca.B = b->B;
-  ca.err = ctx->err_dev;
-  if ((rc = launch_compact(ctx, ca, b->S))) return rc;
-  if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[2], st));
-  // K4
-  LogitsArgs la{};
-  la.H = in->hidden;
-  la.d = b->d;
-  la.R_total = R;
-  la.Bsent = b->B;
-  la.E = b->model->E;
-  la.bias = b->model->bias;
-  la.n_shared = b->n_shared;
-  la.ids = b->cmode == 0 ? b->ids : nullptr;
-  la.ncap = b->ncap;
-  la.n_cand = b->n_cand;
-  la.S = b->S;
-  la.out = b->logits;
-  la.ldo = b->ncap;
-  if ((rc = launch_logits(ctx, la, b->mode, ctx->sm_count * 8))) return rc;
-  if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[3], st));
+  lsb_status rc = step_front(b, in, 1);
+  if (rc) return rc;
   // K5a
   SoftmaxArgs sa{};
   sa.logits = b->logits;

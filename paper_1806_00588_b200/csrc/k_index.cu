@@ -387,7 +387,7 @@ lsb_status launch_wta_hash(lsb_ctx* ctx, const float* M, long long n, int d,
     set_error("wta_hash: row of dimension " + std::to_string(d) + " exceeds shared memory");
     return LSB_EINVAL;
   }
-  if (smem > 48 * 1024)
+  if (smem > 0)
     LSB_CUDA(cudaFuncSetAttribute(k_wta_hash_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
   const long long blocks_needed = (n + warps - 1) / warps;

@@ -150,7 +150,7 @@ lsb_status launch_softmax(lsb_ctx* ctx, const SoftmaxArgs& a) {
   const size_t smem = static_cast<size_t>(std::max(a.topB, 1)) * kSelT * 8;
   if (smem > ctx->smem_optin) return set_error("softmax: beam too large"), LSB_EINVAL;
   static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
+  if (smem > configured) {
     LSB_CUDA(cudaFuncSetAttribute(k_softmax_topb, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     configured = smem;
@@ -434,7 +434,7 @@ lsb_status launch_expand(lsb_ctx* ctx, const ExpandArgs& a) {
   const size_t rank_smem = static_cast<size_t>(nl) * std::max(a.topB, 1) * (8 + 8 + 4);
   if (nl <= kRankMaxLists && rank_smem <= ctx->smem_optin) {
     static size_t configured = 0;
-    if (rank_smem > 48 * 1024 && rank_smem > configured) {
+    if (rank_smem > configured) {
       LSB_CUDA(cudaFuncSetAttribute(k_expand, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(rank_smem)));
       configured = rank_smem;
@@ -446,7 +446,7 @@ lsb_status launch_expand(lsb_ctx* ctx, const ExpandArgs& a) {
   const size_t smem = static_cast<size_t>(nl) * (8 + 8 + 4 + 4 + 4) + 16;
   if (smem > ctx->smem_optin) return set_error("expand: too many rows"), LSB_EINVAL;
   static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
+  if (smem > configured) {
     LSB_CUDA(cudaFuncSetAttribute(k_expand_tournament,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));

@@ -118,7 +118,7 @@ lsb_status launch_probe(lsb_ctx* ctx, const ProbeArgs& a) {
     return LSB_EINVAL;
   }
   static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
+  if (smem > configured) {
     LSB_CUDA(cudaFuncSetAttribute(k_probe_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     configured = smem;
@@ -256,7 +256,7 @@ lsb_status launch_compact(lsb_ctx* ctx, const CompactArgs& a, int S) {
   const size_t smem = static_cast<size_t>(a.nwords) * 4;
   if (smem > ctx->smem_optin) return set_error("compact: vocabulary too large"), LSB_EINVAL;
   static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
+  if (smem > configured) {
     LSB_CUDA(cudaFuncSetAttribute(k_compact, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     configured = smem;

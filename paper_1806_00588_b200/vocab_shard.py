@@ -1,0 +1,144 @@
+"""Vocabulary-sharded decode step (BASELINE cfg 4: |V| = 200k, d = 1024).
+
+Rank g of G owns the contiguous vocabulary slice [v_g, v_g + n_g) of E: its
+own device copy of that slice, a band index over it built with the global
+permutation seed (a word's band codes -- hence its hit counts -- do not
+depend on the other words), and a fused-step batch whose top-T prefix and
+specials are shifted into the slice. One decode step is the three device
+phases of include/lshbeam_b200.h §8 separated by two all-gathers over the
+ranks (NCCL over NVLink in production, gloo in the CPU tests):
+
+  phase1 -> all_gather(row max)                       4 B per row per rank
+  phase2 -> all_gather(row exp-sum), all_gather(top-B' lists)
+                                                      8 + 8*B' B per row per rank
+  phase3 -> identical choices + hidden reorder on every rank
+
+At S=64, B=12 that is 768 rows x 140 B ~ 105 KB per rank per step: the
+exchange is latency-bound, so it is two collectives per step, batched over
+all sentences. The reference has no multi-device path; results equal the
+unsharded step bit for bit in PARITY mode (tests/test_gpu_vocab_shard.py).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+from . import _native as N
+from .lshbeam import PARITY, Batch, Index, Model
+
+
+def shard_bounds(V: int, G: int, g: int) -> tuple[int, int]:
+    """Contiguous split of [0, V): the first V % G ranks take one extra word."""
+    base, rem = divmod(V, G)
+    n = base + (1 if g < rem else 0)
+    v0 = g * base + min(g, rem)
+    return v0, n
+
+
+def local_config(T: int, specials, v0: int, n: int):
+    """The slice's view of the global candidate rules: [0, T) becomes
+    [0, clamp(T - v0, 0, n)) and specials outside the slice drop out."""
+    T_local = max(0, min(T - v0, n))
+    sp = sorted({int(s) - v0 for s in specials if v0 <= int(s) < v0 + n})
+    return T_local, sp
+
+
+class VocabShard:
+    """One rank's share: slice model + slice index + a batch over the slice.
+
+    ``E_slice`` / ``bias_slice`` are torch CUDA tensors on the context's
+    device ([n, d] fp32 / [n] fp32); they are copied into the model."""
+
+    def __init__(self, ctx, E_slice, bias_slice, v0: int, V: int, K: int, u: int, W: int,
+                 perm_seed: int, index_seed: int, S: int, B: int, T: int, t: int, specials=(),
+                 mode: int = PARITY):
+        import torch
+        n, d = E_slice.shape
+        self.ctx, self.lib = ctx, ctx.lib
+        self.v0, self.n, self.V, self.S, self.B = v0, n, V, S, B
+        self.model = Model(ctx, None, device_ptrs=(E_slice.data_ptr(),
+                                                   bias_slice.data_ptr() if bias_slice is not None else None,
+                                                   n, d))
+        self.index = Index(ctx, self.model, K=K, u=u, W=W, perm_seed=perm_seed,
+                           index_seed=index_seed)
+        T_local, sp = local_config(T, specials, v0, n)
+        self.batch = Batch(ctx, self.model, self.index, S=S, B=B, T=T_local, t=t, specials=sp,
+                           mode=mode)
+        self.width = int(self.lib.lsb_shard_width(self.batch.h))
+        R = S * B
+        dev = torch.device("cuda", ctx.device)
+        self.rowmax = torch.empty(R, dtype=torch.float32, device=dev)
+        self.rowsum = torch.empty(R, dtype=torch.float64, device=dev)
+        # lsb_shard_top is {float, uint32}: 8 bytes, carried as int64 words
+        self.top = torch.empty(R * self.width, dtype=torch.int64, device=dev)
+
+    @staticmethod
+    def _state(hidden, scores, finished, n_hyp):
+        p = lambda x: x.data_ptr() if x is not None else None
+        return N.lsb_state_dev(p(hidden), p(scores), p(finished), p(n_hyp))
+
+    def phase1(self, st):
+        N.check(self.lib.lsb_shard_phase1(self.batch.h, C.byref(st), self.rowmax.data_ptr()),
+                "lsb_shard_phase1")
+
+    def phase2(self, st, allmax, G: int):
+        N.check(self.lib.lsb_shard_phase2(self.batch.h, C.byref(st), allmax.data_ptr(), G,
+                                          self.v0, self.rowsum.data_ptr(), self.top.data_ptr()),
+                "lsb_shard_phase2")
+
+    def phase3(self, st, allsum, alltop, G: int, choices, n_choices, hidden_out=None):
+        out = N.lsb_out_dev(choices.data_ptr(), n_choices.data_ptr(),
+                            hidden_out.data_ptr() if hidden_out is not None else None)
+        N.check(self.lib.lsb_shard_phase3(self.batch.h, C.byref(st), allsum.data_ptr(),
+                                          alltop.data_ptr(), G, C.byref(out)),
+                "lsb_shard_phase3")
+
+    def close(self):
+        for x in (self.batch, self.index, self.model):
+            x.close()
+
+
+def _gather(x, G: int, group):
+    """all_gather in rank order into a flat buffer (the layout gloo and NCCL
+    both accept), viewed as [G, *x.shape]."""
+    import torch
+    import torch.distributed as dist
+    out = torch.empty(G * x.numel(), dtype=x.dtype, device=x.device)
+    dist.all_gather_into_tensor(out, x.reshape(-1), group=group)
+    return out.view((G,) + tuple(x.shape))
+
+
+def sharded_step(shard, hidden, scores, finished, n_hyp, choices, n_choices, hidden_out=None,
+                 group=None):
+    """One vocabulary-sharded step on this rank (torch.distributed must be
+    initialised; the shard's context must run on torch's current stream so
+    the collectives are ordered after the phases)."""
+    import torch
+    import torch.distributed as dist
+    G = dist.get_world_size(group)
+    st = shard._state(hidden, scores, finished, n_hyp)
+    shard.phase1(st)
+    allmax = _gather(shard.rowmax, G, group)
+    shard.phase2(st, allmax, G)
+    allsum = _gather(shard.rowsum, G, group)
+    alltop = _gather(shard.top, G, group)
+    shard.phase3(st, allsum, alltop, G, choices, n_choices, hidden_out)
+
+
+def local_sharded_step(shards, hidden, scores, finished, n_hyp, choices, n_choices,
+                       hidden_out=None):
+    """The same protocol for G shards held by ONE process (one GPU): the
+    all-gathers become stacks in rank order. Used by the single-GPU parity
+    tests and the 1-GPU cfg-4 bench; every shard writes the same outputs, the
+    last one's are kept."""
+    import torch
+    G = len(shards)
+    sts = [s._state(hidden, scores, finished, n_hyp) for s in shards]
+    for s, st in zip(shards, sts):
+        s.phase1(st)
+    allmax = torch.stack([s.rowmax for s in shards])
+    for s, st in zip(shards, sts):
+        s.phase2(st, allmax, G)
+    allsum = torch.stack([s.rowsum for s in shards])
+    alltop = torch.stack([s.top for s in shards])
+    for s, st in zip(shards, sts):
+        s.phase3(st, allsum, alltop, G, choices, n_choices, hidden_out)
