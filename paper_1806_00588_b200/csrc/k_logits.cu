@@ -5,7 +5,7 @@
 // E_LSH is never materialised: each CTA owns RB hypothesis rows x 128*CB
 // candidate columns and streams the candidates' embedding rows straight from
 // E (row gather by id) into shared memory with cp.async, d in chunks of 32
-// floats through a 3-stage ring, so the inner loop reads only shared memory:
+// floats through a 2-stage ring (5 CTAs per SM), so the inner loop reads only shared memory:
 // the H row chunk as a warp-wide broadcast and each thread's own E row with
 // conflict-free 16-byte loads (row pitch 36 floats = 4 mod 32 banks).
 //
@@ -31,7 +31,7 @@ namespace lsb {
 constexpr int kLT = 128;        // threads per CTA
 constexpr int kKC = 32;         // floats of d per pipeline stage
 constexpr int kKS = kKC + 4;    // shared-memory row pitch in floats
-constexpr int kStages = 3;
+constexpr int kStages = 2;
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
@@ -54,8 +54,39 @@ constexpr size_t logits_smem_bytes() {
   return static_cast<size_t>(kStages) * (kLT * CB + RB) * kKS * 4 + kLT * CB * 4;
 }
 
+// One 4-wide step of d for RB rows x CB columns: float4 of H (smem
+// broadcast) times float4 of each column's E row.
+template <int RB, int CB, bool PARITY>
+__device__ __forceinline__ void mac4(float (&acc)[RB][CB][PARITY ? 4 : 1], const float* Es,
+                                     const float* Hs, int tid, int k4) {
+  float4 e[CB];
+#pragma unroll
+  for (int cb = 0; cb < CB; ++cb)
+    e[cb] = *reinterpret_cast<const float4*>(Es + (tid + cb * kLT) * kKS + k4 * 4);
+#pragma unroll
+  for (int rb = 0; rb < RB; ++rb) {
+    const float4 h = *reinterpret_cast<const float4*>(Hs + rb * kKS + k4 * 4);
+#pragma unroll
+    for (int cb = 0; cb < CB; ++cb) {
+      if constexpr (PARITY) {
+        acc[rb][cb][0] = __fadd_rn(acc[rb][cb][0], __fmul_rn(h.x, e[cb].x));
+        acc[rb][cb][1] = __fadd_rn(acc[rb][cb][1], __fmul_rn(h.y, e[cb].y));
+        acc[rb][cb][2] = __fadd_rn(acc[rb][cb][2], __fmul_rn(h.z, e[cb].z));
+        acc[rb][cb][3] = __fadd_rn(acc[rb][cb][3], __fmul_rn(h.w, e[cb].w));
+      } else {
+        float x = acc[rb][cb][0];
+        x = fmaf(h.x, e[cb].x, x);
+        x = fmaf(h.y, e[cb].y, x);
+        x = fmaf(h.z, e[cb].z, x);
+        x = fmaf(h.w, e[cb].w, x);
+        acc[rb][cb][0] = x;
+      }
+    }
+  }
+}
+
 template <int RB, int CB, bool PARITY, bool VEC>
-__global__ void __launch_bounds__(kLT) k_logits(LogitsArgs a) {
+__global__ void __launch_bounds__(kLT, PARITY ? 5 : 4) k_logits(LogitsArgs a) {
   extern __shared__ __align__(16) float sm[];
   constexpr int CT = kLT * CB;
   constexpr int STAGE = (CT + RB) * kKS;
@@ -162,32 +193,11 @@ __global__ void __launch_bounds__(kLT) k_logits(LogitsArgs a) {
       const float* Hs = Es + CT * kKS;
       const int kv = max(0, min(kKC, d4 - kc * kKC)) >> 2;  // full 4-lane groups
       if (warp_live) {
-#pragma unroll 4
-        for (int k4 = 0; k4 < kv; ++k4) {
-          float4 e[CB];
+        if (kv == kKC / 4) {
 #pragma unroll
-          for (int cb = 0; cb < CB; ++cb)
-            e[cb] = *reinterpret_cast<const float4*>(Es + (tid + cb * kLT) * kKS + k4 * 4);
-#pragma unroll
-          for (int rb = 0; rb < RB; ++rb) {
-            const float4 h = *reinterpret_cast<const float4*>(Hs + rb * kKS + k4 * 4);
-#pragma unroll
-            for (int cb = 0; cb < CB; ++cb) {
-              if constexpr (PARITY) {
-                acc[rb][cb][0] = __fadd_rn(acc[rb][cb][0], __fmul_rn(h.x, e[cb].x));
-                acc[rb][cb][1] = __fadd_rn(acc[rb][cb][1], __fmul_rn(h.y, e[cb].y));
-                acc[rb][cb][2] = __fadd_rn(acc[rb][cb][2], __fmul_rn(h.z, e[cb].z));
-                acc[rb][cb][3] = __fadd_rn(acc[rb][cb][3], __fmul_rn(h.w, e[cb].w));
-              } else {
-                float x = acc[rb][cb][0];
-                x = fmaf(h.x, e[cb].x, x);
-                x = fmaf(h.y, e[cb].y, x);
-                x = fmaf(h.z, e[cb].z, x);
-                x = fmaf(h.w, e[cb].w, x);
-                acc[rb][cb][0] = x;
-              }
-            }
-          }
+          for (int k4 = 0; k4 < kKC / 4; ++k4) mac4<RB, CB, PARITY>(acc, Es, Hs, tid, k4);
+        } else {
+          for (int k4 = 0; k4 < kv; ++k4) mac4<RB, CB, PARITY>(acc, Es, Hs, tid, k4);
         }
       }
     }
