@@ -31,6 +31,9 @@ struct lsb_batch {
   float* logits = nullptr;
   lsb::TopEntry* top = nullptr;
   int32_t* top_n = nullptr;
+  float* tc_A = nullptr;        // FAST: pre-tiled E[0, n_shared) for tcgen05
+  float* tc_H = nullptr;        // FAST: per-step tiled H
+  int tc_N = 0;
   lsb::TopEntry* sh_top = nullptr;   // vocabulary-sharded step: local top-B'
   int32_t* sh_topn = nullptr;
   // staging for lsb_step_host

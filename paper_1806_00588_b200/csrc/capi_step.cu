@@ -27,7 +27,7 @@ lsb_status free_batch(lsb_batch* b) {
   void* ptrs[] = {b->specials, b->qcodes,   b->bitmap,     b->ids,          b->n_cand,
                   b->prov,     b->logits,   b->top,        b->top_n,        b->h_hidden,
                   b->h_scores, b->h_finished, b->h_nhyp,   b->h_choices,    b->h_nchoices,
-                  b->h_hidden_out, b->sh_top, b->sh_topn};
+                  b->h_hidden_out, b->sh_top, b->sh_topn, b->tc_A, b->tc_H};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : b->ring)
@@ -104,6 +104,9 @@ lsb_status lsb::step_front(lsb_batch* b, const lsb_state_dev* in, int empty_is_e
   la.S = b->S;
   la.out = b->logits;
   la.ldo = b->ncap;
+  la.tc_A = b->tc_A;
+  la.tc_H = b->tc_H;
+  la.tc_N = b->tc_N;
   if ((rc = launch_logits(ctx, la, b->mode, ctx->sm_count * 8))) return rc;
   if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[3], st));
   return LSB_OK;
@@ -172,6 +175,18 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
   if (e == cudaSuccess) e = dalloc(&b->logits, SB * b->ncap);
   if (e == cudaSuccess) e = dalloc(&b->top, SB * b->B);
   if (e == cudaSuccess) e = dalloc(&b->top_n, SB);
+  // FAST: the rows sharing [0, n_shared) form a dense contraction for the
+  // tensor cores; E's block is split into 3xTF32 and tiled once, here
+  const int R = b->S * b->B;
+  if (e == cudaSuccess && b->mode == LSB_MODE_FAST && R >= kTcMinRows && b->n_shared > 0 &&
+      (b->d & 3) == 0 && (reinterpret_cast<uintptr_t>(model->E) & 15) == 0) {
+    b->tc_N = tc_rows_per_tile(ctx, R, b->n_shared);
+    e = dalloc(&b->tc_A, tf32_tiled_floats(static_cast<int>(b->n_shared), b->d, 128));
+    if (e == cudaSuccess) e = dalloc(&b->tc_H, tf32_tiled_floats(R, b->d, b->tc_N));
+    if (e == cudaSuccess &&
+        launch_tf32_tile(ctx, model->E, static_cast<int>(b->n_shared), b->d, 128, b->tc_A) != LSB_OK)
+      e = cudaGetLastError();
+  }
   if (e != cudaSuccess) {
     free_batch(b);
     return cuda_status(e, "lsb_batch_create");

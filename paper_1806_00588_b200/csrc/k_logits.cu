@@ -23,6 +23,7 @@
 // src/beam_decoder.cpp:34-42 -> bit-identical logits. FAST uses one FFMA
 // chain per output.
 #include <algorithm>
+#include <cstdlib>
 
 #include "k_step.cuh"
 
@@ -31,7 +32,6 @@ namespace lsb {
 constexpr int kLT = 128;        // threads per CTA
 constexpr int kKC = 32;         // floats of d per pipeline stage
 constexpr int kKS = kKC + 4;    // shared-memory row pitch in floats
-constexpr int kStages = 2;
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
@@ -49,9 +49,9 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-template <int RB, int CB>
+template <int RB, int CB, int NS>
 constexpr size_t logits_smem_bytes() {
-  return static_cast<size_t>(kStages) * (kLT * CB + RB) * kKS * 4 + kLT * CB * 4;
+  return static_cast<size_t>(NS) * (kLT * CB + RB) * kKS * 4 + kLT * CB * 4;
 }
 
 // One 4-wide step of d for RB rows x CB columns: float4 of H (smem
@@ -85,8 +85,8 @@ __device__ __forceinline__ void mac4(float (&acc)[RB][CB][PARITY ? 4 : 1], const
   }
 }
 
-template <int RB, int CB, bool PARITY, bool VEC>
-__global__ void __launch_bounds__(kLT, PARITY ? 5 : 4) k_logits(LogitsArgs a) {
+template <int RB, int CB, bool PARITY, bool VEC, int kStages>
+__global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs a) {
   extern __shared__ __align__(16) float sm[];
   constexpr int CT = kLT * CB;
   constexpr int STAGE = (CT + RB) * kKS;
@@ -129,26 +129,38 @@ __global__ void __launch_bounds__(kLT, PARITY ? 5 : 4) k_logits(LogitsArgs a) {
       sid[c] = c < ncols ? (list ? __ldg(list + t0 + c) : t0 + c) : 0u;
     __syncthreads();
 
+    // per-tile source offsets (elements) of this thread's 16-byte pieces:
+    // piece i covers column (tid >> 3) + 16 i, floats [4 (tid & 7), +4) of
+    // every chunk; invalid columns / rows carry bit 31 and are zero-filled
+    const int part = tid & 7;
+    uint32_t eoff[VEC ? 8 * CB : 1];
+    if constexpr (VEC) {
+#pragma unroll
+      for (int i = 0; i < 8 * CB; ++i) {
+        const int col = (tid >> 3) + 16 * i;
+        eoff[i] = col < ncols ? sid[col] * static_cast<uint32_t>(d) + part * 4 : 0x80000000u;
+      }
+    }
+    const int hrow = tid >> 3;
+    const uint32_t hoff = (tid < RB * 8 && row0 + hrow < rowlim)
+                              ? static_cast<uint32_t>(row0 + hrow) * d + part * 4
+                              : 0x80000000u;
+
     auto load_chunk = [&](int stage, int kc) {
       float* Es = sm + stage * STAGE;
       float* Hs = Es + CT * kKS;
       const int c0 = kc * kKC;
       if constexpr (VEC) {
+        const bool kin = c0 + part * 4 < d;
 #pragma unroll
         for (int i = 0; i < 8 * CB; ++i) {
-          const int q = tid + kLT * i;
-          const int col = q >> 3, part = q & 7;
-          const int k = c0 + part * 4;
-          const bool ok = col < ncols && k < d;
-          const float* src = ok ? a.E + static_cast<size_t>(sid[col]) * d + k : a.E;
-          cp_async16(Es + col * kKS + part * 4, src, ok ? 16 : 0);
+          const bool ok = kin && !(eoff[i] & 0x80000000u);
+          cp_async16(Es + ((tid >> 3) + 16 * i) * kKS + part * 4, a.E + (ok ? eoff[i] + c0 : 0),
+                     ok ? 16 : 0);
         }
-        for (int q = tid; q < RB * 8; q += kLT) {
-          const int rb = q >> 3, part = q & 7;
-          const int k = c0 + part * 4;
-          const bool ok = row0 + rb < rowlim && k < d;
-          const float* src = ok ? a.H + static_cast<size_t>(row0 + rb) * d + k : a.H;
-          cp_async16(Hs + rb * kKS + part * 4, src, ok ? 16 : 0);
+        if (tid < RB * 8) {
+          const bool ok = kin && !(hoff & 0x80000000u);
+          cp_async16(Hs + hrow * kKS + part * 4, a.H + (ok ? hoff + c0 : 0), ok ? 16 : 0);
         }
       } else {
         for (int q = tid; q < CT * kKC; q += kLT) {
@@ -263,17 +275,17 @@ int choose_rb(int B) {
   return best;
 }
 
-template <int RB, int CB, bool PARITY, bool VEC>
+template <int RB, int CB, bool PARITY, bool VEC, int NS>
 static lsb_status launch_variant(lsb_ctx* ctx, const LogitsArgs& a, int grid) {
-  constexpr size_t smem = logits_smem_bytes<RB, CB>();
+  constexpr size_t smem = logits_smem_bytes<RB, CB, NS>();
   static bool configured = false;
   if (!configured) {
-    LSB_CUDA(cudaFuncSetAttribute(k_logits<RB, CB, PARITY, VEC>,
+    LSB_CUDA(cudaFuncSetAttribute(k_logits<RB, CB, PARITY, VEC, NS>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     configured = true;
   }
-  k_logits<RB, CB, PARITY, VEC><<<grid, kLT, smem, ctx->stream>>>(a);
+  k_logits<RB, CB, PARITY, VEC, NS><<<grid, kLT, smem, ctx->stream>>>(a);
   LSB_LAUNCHED(ctx, "k_logits");
   return LSB_OK;
 }
@@ -283,7 +295,7 @@ static lsb_status launch_logits_rb(lsb_ctx* ctx, LogitsArgs a, int target) {
   constexpr int CT = kLT * CB;
   const int rgroups = (a.R_total + RB - 1) / RB;
   a.ctiles_shared = static_cast<int>((a.n_shared + CT - 1) / CT);
-  a.jobs_shared = a.n_shared ? rgroups * a.ctiles_shared : 0;
+  a.jobs_shared = (a.n_shared && !a.skip_shared) ? rgroups * a.ctiles_shared : 0;
   a.G = (a.Bsent + RB - 1) / RB;
   if (a.ids && a.S > 0) {
     const size_t max_tiles = (a.ncap > a.n_shared ? a.ncap - a.n_shared : 0) / CT + 1;
@@ -296,18 +308,41 @@ static lsb_status launch_logits_rb(lsb_ctx* ctx, LogitsArgs a, int target) {
   if (grid == 0) return LSB_OK;
   const bool vec = (a.d & 3) == 0 && (reinterpret_cast<uintptr_t>(a.E) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(a.H) & 15) == 0;
-  return vec ? launch_variant<RB, CB, PARITY, true>(ctx, a, grid)
-             : launch_variant<RB, CB, PARITY, false>(ctx, a, grid);
+  // Survivor-only launches (the shared block went to the tensor cores) have
+  // no other CTAs to hide their L2 latency behind: 3-stage ring instead of 2.
+  if (a.skip_shared)
+    return vec ? launch_variant<RB, CB, PARITY, true, 3>(ctx, a, grid)
+               : launch_variant<RB, CB, PARITY, false, 3>(ctx, a, grid);
+  return vec ? launch_variant<RB, CB, PARITY, true, 2>(ctx, a, grid)
+             : launch_variant<RB, CB, PARITY, false, 2>(ctx, a, grid);
 }
 
-// PARITY: one column per thread (8 FP instructions per 16-byte E load keep
-// shared-memory wavefronts under the FMUL/FADD issue rate). FAST does half
-// the FP work per load, so it takes two columns per thread.
+// One column per thread, RB rows: 8 FP instructions (PARITY) or 4 FFMA
+// (FAST) per 16-byte E load; 5 CTAs per SM.
 lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_ctas) {
   const bool fast = mode == LSB_MODE_FAST;
+  // FAST + enough rows sharing the identity columns [0, n_shared): a dense
+  // contraction -> tcgen05 tensor cores; the per-sentence survivors stay on
+  // the FFMA kernel below.
+  static const bool tc_off = getenv("LSB_NO_TC") != nullptr;
+  if (fast && !tc_off && a.n_shared > 0 && a.R_total >= kTcMinRows && (a.d & 3) == 0 &&
+      (reinterpret_cast<uintptr_t>(a.E) & 15) == 0 && (reinterpret_cast<uintptr_t>(a.H) & 15) == 0) {
+    lsb_status rc;
+    if (a.tc_A && a.tc_H) {
+      rc = launch_tf32_tile(ctx, a.H, a.R_total, a.d, a.tc_N, a.tc_H);
+      if (!rc)
+        rc = launch_tc_logits_tiled(ctx, a.tc_A, a.tc_H, a.tc_N, a.R_total, a.d, a.bias, 0,
+                                    a.n_shared, a.out, a.ldo, 0);
+    } else {
+      rc = launch_tc_logits(ctx, a.H, a.R_total, a.E, a.bias, a.d, 0, a.n_shared, a.out, a.ldo, 0);
+    }
+    if (rc) return rc;
+    a.skip_shared = 1;
+    if (!a.ids || a.S == 0) return LSB_OK;
+  }
 #define LSB_RB(R)                                                        \
   case R:                                                                \
-    return fast ? launch_logits_rb<R, 2, false>(ctx, a, target_ctas)     \
+    return fast ? launch_logits_rb<R, 1, false>(ctx, a, target_ctas)     \
                 : launch_logits_rb<R, 1, true>(ctx, a, target_ctas);
   switch (choose_rb(a.Bsent)) {
     LSB_RB(16)
@@ -318,7 +353,7 @@ lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_c
     LSB_RB(4)
     LSB_RB(2)
     default:
-      return fast ? launch_logits_rb<1, 2, false>(ctx, a, target_ctas)
+      return fast ? launch_logits_rb<1, 1, false>(ctx, a, target_ctas)
                   : launch_logits_rb<1, 1, true>(ctx, a, target_ctas);
   }
 #undef LSB_RB

@@ -59,6 +59,10 @@ struct LogitsArgs {
   int jobs_shared, ctiles_shared;
   float* out;              // [R_total][ldo]
   size_t ldo;
+  int skip_shared;         // the shared block was scored elsewhere (tensor cores)
+  const float* tc_A;       // FAST: E[0, n_shared) pre-tiled for tcgen05 (or null)
+  float* tc_H;             // FAST: scratch for the per-step tiled H
+  int tc_N;                // rows per tcgen05 tile the scratch was sized for
 };
 
 // K5a: row softmax + per-row top-B by (p desc, column asc).
@@ -105,6 +109,19 @@ struct ExpandArgs {
 lsb_status launch_probe(lsb_ctx* ctx, const ProbeArgs& a);
 lsb_status launch_compact(lsb_ctx* ctx, const CompactArgs& a, int S);
 lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_ctas);
+// Tensor-core (tcgen05, 3xTF32) logits for rows x identity columns
+// [col0, col0 + ncols) of E; FAST mode only.
+lsb_status launch_tc_logits(lsb_ctx* ctx, const float* H, int rows, const float* E,
+                            const float* bias, int d, uint32_t col0, uint32_t ncols, float* out,
+                            size_t ldo, uint32_t out_col0);
+// Pre-tiled variant (operands from launch_tf32_tile with R = 128 / N).
+lsb_status launch_tc_logits_tiled(lsb_ctx* ctx, const float* A_tiled, const float* H_tiled,
+                                  int N, int rows, int d, const float* bias, uint32_t col0,
+                                  uint32_t ncols, float* out, size_t ldo, uint32_t out_col0);
+lsb_status launch_tf32_tile(lsb_ctx* ctx, const float* src, int nrows, int d, int R, float* out);
+size_t tf32_tiled_floats(int nrows, int d, int R);
+int tc_rows_per_tile(lsb_ctx* ctx, int rows, uint32_t ncols);
+constexpr int kTcMinRows = 64;  // rows sharing a column block before tensor cores pay
 lsb_status launch_softmax(lsb_ctx* ctx, const SoftmaxArgs& a);
 lsb_status launch_expand(lsb_ctx* ctx, const ExpandArgs& a);
 
