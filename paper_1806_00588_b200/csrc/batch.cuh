@@ -31,6 +31,7 @@ struct lsb_batch {
   float* logits = nullptr;
   lsb::TopEntry* top = nullptr;
   int32_t* top_n = nullptr;
+  uint32_t* arrive = nullptr;   // fused K5: per-sentence arrival counters (zeroed)
   float* tc_A = nullptr;        // FAST: pre-tiled E[0, n_shared) for tcgen05
   float* tc_H = nullptr;        // FAST: per-step tiled H
   int tc_N = 0;

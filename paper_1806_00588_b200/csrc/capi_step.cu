@@ -6,6 +6,7 @@
 //   K1+K2 k_probe_count -> K3 k_compact -> K4 k_logits -> K5a k_softmax_topb
 //   -> K5b k_expand.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -27,7 +28,7 @@ lsb_status free_batch(lsb_batch* b) {
   void* ptrs[] = {b->specials, b->qcodes,   b->bitmap,     b->ids,          b->n_cand,
                   b->prov,     b->logits,   b->top,        b->top_n,        b->h_hidden,
                   b->h_scores, b->h_finished, b->h_nhyp,   b->h_choices,    b->h_nchoices,
-                  b->h_hidden_out, b->sh_top, b->sh_topn, b->tc_A, b->tc_H};
+                  b->h_hidden_out, b->sh_top, b->sh_topn, b->tc_A, b->tc_H, b->arrive};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : b->ring)
@@ -175,6 +176,8 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
   if (e == cudaSuccess) e = dalloc(&b->logits, SB * b->ncap);
   if (e == cudaSuccess) e = dalloc(&b->top, SB * b->B);
   if (e == cudaSuccess) e = dalloc(&b->top_n, SB);
+  if (e == cudaSuccess) e = dalloc(&b->arrive, b->S);
+  if (e == cudaSuccess) e = cudaMemset(b->arrive, 0, b->S * sizeof(uint32_t));
   // FAST: the rows sharing [0, n_shared) form a dense contraction for the
   // tensor cores; E's block is split into 3xTF32 and tiled once, here
   const int R = b->S * b->B;
@@ -256,7 +259,7 @@ lsb_status lsb_step(lsb_batch* b, const lsb_state_dev* in, const lsb_out_dev* ou
   const int R = b->S * b->B;
   lsb_status rc = step_front(b, in, 1);
   if (rc) return rc;
-  // K5a
+  // K5a + K5b
   SoftmaxArgs sa{};
   sa.logits = b->logits;
   sa.ldl = b->ncap;
@@ -270,9 +273,6 @@ lsb_status lsb_step(lsb_batch* b, const lsb_state_dev* in, const lsb_out_dev* ou
   sa.top = b->top;
   sa.top_n = b->top_n;
   sa.err = ctx->err_dev;
-  if ((rc = launch_softmax(ctx, sa))) return rc;
-  if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[4], st));
-  // K5b
   ExpandArgs ea{};
   ea.S = b->S;
   ea.Bsent = b->B;
@@ -290,7 +290,28 @@ lsb_status lsb_step(lsb_batch* b, const lsb_state_dev* in, const lsb_out_dev* ou
   ea.hidden_out = out->hidden_out;
   ea.choices = out->choices;
   ea.n_choices = out->n_choices;
-  if ((rc = launch_expand(ctx, ea))) return rc;
+  // K5 variant (LSB_K5): 0 = CTA-per-row softmax + per-sentence expansion
+  // (default; measured fastest with the K5b reorder batched), 1 = warp-per-row
+  // softmax + expansion, 2 = one fused launch per sentence. All three are
+  // bit-identical (tests/test_gpu_step.py runs under each).
+  static const int k5 = [] {
+    const char* e = getenv("LSB_K5");
+    return e ? atoi(e) : 0;
+  }();
+  if (b->cmode == 0 && k5 == 2 && select_fused_applies(sa, ea)) {
+    // one launch: CTA per sentence, warp per row, then the expansion
+    if ((rc = launch_select_fused(ctx, sa, ea, static_cast<uint32_t>(b->ncap), b->arrive))) return rc;
+    if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[4], st));
+  } else if (b->cmode == 0 && k5 == 1) {
+    // warp per row over the whole GPU, then the per-sentence expansion
+    if ((rc = launch_softmax_warp(ctx, sa, static_cast<uint32_t>(b->ncap)))) return rc;
+    if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[4], st));
+    if ((rc = launch_expand(ctx, ea))) return rc;
+  } else {
+    if ((rc = launch_softmax(ctx, sa))) return rc;
+    if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[4], st));
+    if ((rc = launch_expand(ctx, ea))) return rc;
+  }
   if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[5], st));
   b->last = *in;
   b->has_last = true;

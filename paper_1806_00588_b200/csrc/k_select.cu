@@ -181,22 +181,56 @@ __device__ __forceinline__ long long word_of(const ExpandArgs& a, const uint32_t
 }
 
 // Hidden-state reorder: child k of sentence s starts from its parent's vector.
+// One flat (child, float4) index space; each thread keeps 8 loads in flight
+// before storing (a load->store chain per element would serialise on
+// latency: the store could alias the next load).
 __device__ void reorder_hidden(const ExpandArgs& a, int s, int count, const uint32_t* beams) {
-  // one flat index space over (child, column) so every load is independent
   const int d = a.d;
   const size_t rbase = static_cast<size_t>(s) * a.Bsent;
   const size_t obase = static_cast<size_t>(s) * a.topB;
+  constexpr int U = 8;
   if ((d & 3) == 0) {
     const int d4 = d >> 2;
-    for (int q = threadIdx.x; q < count * d4; q += blockDim.x) {
-      const int k = q / d4, c = q - k * d4;
-      reinterpret_cast<float4*>(a.hidden_out + (obase + k) * d)[c] =
-          __ldg(reinterpret_cast<const float4*>(a.hidden + (rbase + beams[k]) * d) + c);
+    const int total = count * d4;
+    for (int q0 = threadIdx.x; q0 < total; q0 += U * blockDim.x) {
+      float4 t[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = q0 + u * blockDim.x;
+        if (q < total) {
+          const int k = q / d4, c = q - k * d4;
+          t[u] = __ldg(reinterpret_cast<const float4*>(a.hidden + (rbase + beams[k]) * d) + c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = q0 + u * blockDim.x;
+        if (q < total) {
+          const int k = q / d4, c = q - k * d4;
+          reinterpret_cast<float4*>(a.hidden_out + (obase + k) * d)[c] = t[u];
+        }
+      }
     }
   } else {
-    for (int q = threadIdx.x; q < count * d; q += blockDim.x) {
-      const int k = q / d, c = q - k * d;
-      a.hidden_out[(obase + k) * d + c] = __ldg(a.hidden + (rbase + beams[k]) * d + c);
+    const int total = count * d;
+    for (int q0 = threadIdx.x; q0 < total; q0 += U * blockDim.x) {
+      float t[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = q0 + u * blockDim.x;
+        if (q < total) {
+          const int k = q / d, c = q - k * d;
+          t[u] = __ldg(a.hidden + (rbase + beams[k]) * d + c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = q0 + u * blockDim.x;
+        if (q < total) {
+          const int k = q / d, c = q - k * d;
+          a.hidden_out[(obase + k) * d + c] = t[u];
+        }
+      }
     }
   }
 }
@@ -426,6 +460,307 @@ __global__ void k_expand_tournament(ExpandArgs a) {
   }
   __syncthreads();
   if (a.hidden_out && a.hidden) reorder_hidden(a, s, min(s_count, 64), s_beams);
+}
+
+// ============================================================ fused K5a+K5b
+// The LSH step's rows are short (|V_LSH| ~ 1-2k), so one WARP per row keeps
+// the row in registers (KMAX floats per lane): float max, double exp/sum,
+// p = float(e) * float(1/denom), then B rounds of a warp arg-max by
+// (p desc, column asc) -- the lane that owns the winner drops it and
+// rescans its registers. One CTA per sentence: after a barrier the CTA runs
+// the sentence's expansion (rank selection, as k_expand) and the hidden
+// reorder, so K5 is one launch with no top-list round trip through HBM.
+constexpr int kFusedMaxB = 16;
+
+// Row softmax + top-B with the row in registers (n <= 32*KMAX).
+template <int KMAX>
+__device__ __forceinline__ void fused_row_registers(const SoftmaxArgs& sa, int row, float* L,
+                                                    uint32_t n, TopEntry* out, int lane) {
+  const int B = sa.topB;
+  float v[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    const uint32_t c = lane + 32u * k;
+    v[k] = c < n ? L[c] : -INFINITY;
+  }
+  float mx = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) mx = (mx < v[k]) ? v[k] : mx;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float y = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = (mx < y) ? y : mx;
+  }
+  if (n == 0 || (isinf(mx) && mx < 0)) {
+    if (lane == 0) {
+      atomicOr(sa.err, kErrEmptyRow);
+      sa.top_n[row] = 0;
+    }
+    return;
+  }
+  const double dmx = static_cast<double>(mx);
+  double sum = 0.0;
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    if (lane + 32u * k < n) {
+      const double e = exp(static_cast<double>(v[k]) - dmx);
+      v[k] = static_cast<float>(e);
+      sum += e;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float inv = static_cast<float>(1.0 / sum);
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    const uint32_t c = lane + 32u * k;
+    if (c < n) {
+      v[k] = __fmul_rn(v[k], inv);
+      if (sa.keep_probs) L[c] = v[k];
+    } else {
+      v[k] = -1.0f;  // below every probability
+    }
+  }
+  // lane-local best: strict '>' in ascending k keeps the smallest column
+  float bp = -1.0f;
+  int bk = 0;
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k)
+    if (v[k] > bp) {
+      bp = v[k];
+      bk = k;
+    }
+  const int keep = static_cast<int>(min(static_cast<uint32_t>(B), n));
+  for (int r = 0; r < keep; ++r) {
+    float p = bp;
+    uint32_t col = lane + 32u * bk;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float yp = __shfl_xor_sync(0xffffffffu, p, o);
+      const uint32_t yc = __shfl_xor_sync(0xffffffffu, col, o);
+      if (top_better(yp, yc, p, col)) {
+        p = yp;
+        col = yc;
+      }
+    }
+    if (lane == 0) out[r] = TopEntry{p, col};
+    if ((col & 31u) == static_cast<uint32_t>(lane)) {  // the owner drops it, rescans
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (k == bk) v[k] = -1.0f;
+      bp = -1.0f;
+      bk = 0;
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (v[k] > bp) {
+          bp = v[k];
+          bk = k;
+        }
+    }
+  }
+  if (lane == 0) sa.top_n[row] = keep;
+}
+
+// Same for rows too long for registers: the row stays in global memory and
+// round r takes the best entry strictly below round r-1's winner.
+__device__ void fused_row_global(const SoftmaxArgs& sa, int row, float* L, uint32_t n,
+                                 TopEntry* out, int lane) {
+  const int B = sa.topB;
+  float mx = -INFINITY;
+  for (uint32_t c = lane; c < n; c += 32) mx = (mx < L[c]) ? L[c] : mx;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float y = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = (mx < y) ? y : mx;
+  }
+  if (n == 0 || (isinf(mx) && mx < 0)) {
+    if (lane == 0) {
+      atomicOr(sa.err, kErrEmptyRow);
+      sa.top_n[row] = 0;
+    }
+    return;
+  }
+  const double dmx = static_cast<double>(mx);
+  double sum = 0.0;
+  for (uint32_t c = lane; c < n; c += 32) {
+    const double e = exp(static_cast<double>(L[c]) - dmx);
+    L[c] = static_cast<float>(e);
+    sum += e;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float inv = static_cast<float>(1.0 / sum);
+  for (uint32_t c = lane; c < n; c += 32) L[c] = __fmul_rn(L[c], inv);  // probabilities
+  const int keep = static_cast<int>(min(static_cast<uint32_t>(B), n));
+  float pp = INFINITY;
+  uint32_t pc = 0xFFFFFFFFu;
+  for (int r = 0; r < keep; ++r) {
+    float bp = -1.0f;
+    uint32_t bc = 0xFFFFFFFFu;
+    for (uint32_t c = lane; c < n; c += 32) {
+      const float p = L[c];
+      if (top_better(pp, pc, p, c) && top_better(p, c, bp, bc)) {
+        bp = p;
+        bc = c;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float yp = __shfl_xor_sync(0xffffffffu, bp, o);
+      const uint32_t yc = __shfl_xor_sync(0xffffffffu, bc, o);
+      if (top_better(yp, yc, bp, bc)) {
+        bp = yp;
+        bc = yc;
+      }
+    }
+    if (lane == 0) out[r] = TopEntry{bp, bc};
+    pp = bp;
+    pc = bc;
+  }
+  if (lane == 0) sa.top_n[row] = keep;
+}
+
+// One CTA per sentence, one warp per hypothesis row (B <= 16 warps): every
+// row's softmax/top-B, then (after one barrier) the sentence's expansion by
+// rank selection and the hidden reorder by the whole CTA.
+template <int KMAX>
+__global__ void __launch_bounds__(kFusedMaxB * 32) k_select_fused(SoftmaxArgs sa, ExpandArgs ea) {
+  __shared__ double s_score[kFusedMaxB * kFusedMaxB];
+  __shared__ long long s_word[kFusedMaxB * kFusedMaxB];
+  __shared__ uint32_t s_beam[kFusedMaxB * kFusedMaxB];
+  __shared__ int s_off[kFusedMaxB + 1];
+  __shared__ uint32_t s_pick[kFusedMaxB];
+  __shared__ int s_count;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int s = blockIdx.x;
+  const int Bs = sa.Bsent, B = sa.topB;
+  const size_t rbase = static_cast<size_t>(s) * Bs;
+  const int nhyp = sa.n_hyp ? sa.n_hyp[s] : Bs;
+  if (w < Bs) {
+    const int row = static_cast<int>(rbase) + w;
+    const bool live = w < nhyp && !(sa.finished && sa.finished[row]);
+    TopEntry* out = sa.top + static_cast<size_t>(row) * B;
+    if (live) {
+      const uint32_t n = sa.n_cand[s];
+      float* L = sa.logits + static_cast<size_t>(row) * sa.ldl;
+      if (n <= 32u * KMAX) fused_row_registers<KMAX>(sa, row, L, n, out, lane);
+      else fused_row_global(sa, row, L, n, out, lane);
+    } else if (lane == 0) {
+      sa.top_n[row] = 0;
+    }
+  }
+  __syncthreads();
+  const uint32_t* ids = ea.ids ? ea.ids + static_cast<size_t>(s) * ea.ncap : nullptr;
+  if (w == 0) {
+    int len = 0;
+    if (lane < Bs && lane < nhyp)
+      len = (ea.finished && ea.finished[rbase + lane]) ? 1 : ea.top_n[rbase + lane];
+    int x = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane < Bs) s_off[lane + 1] = x;
+    if (lane == 0) s_off[0] = 0;
+  }
+  __syncthreads();
+  const int total = s_off[Bs];
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    int l = 0;
+    while (l + 1 < Bs && s_off[l + 1] <= e) ++l;
+    const int j = e - s_off[l];
+    double sc;
+    long long wd;
+    if (ea.finished && ea.finished[rbase + l]) {
+      sc = ea.scores[rbase + l];
+      wd = -1;
+    } else {
+      const TopEntry t = ea.top[(rbase + l) * B + j];
+      sc = ea.scores[rbase + l] + log(static_cast<double>(t.p));
+      wd = word_of(ea, ids, t.r);
+    }
+    s_score[e] = sc;
+    s_word[e] = wd;
+    s_beam[e] = static_cast<uint32_t>(l);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    int own = 0;
+    while (own + 1 < Bs && s_off[own + 1] <= e) ++own;
+    const Cand me{s_score[e], s_beam[e], s_word[e]};
+    int rank = e - s_off[own];
+    for (int l = 0; l < Bs && rank < B; ++l) {
+      if (l == own) continue;
+      int b0 = s_off[l], b1 = s_off[l + 1];
+      while (b0 < b1) {
+        const int mid = (b0 + b1) >> 1;
+        if (cand_better(Cand{s_score[mid], s_beam[mid], s_word[mid]}, me)) b0 = mid + 1;
+        else b1 = mid;
+      }
+      rank += b0 - s_off[l];
+    }
+    if (rank < B) {
+      ea.choices[static_cast<size_t>(s) * B + rank] =
+          lsb_choice{me.score, me.beam, 0u, static_cast<int64_t>(me.word)};
+      s_pick[rank] = me.beam;
+    }
+  }
+  if (threadIdx.x == 0) {
+    s_count = min(B, total);
+    ea.n_choices[s] = s_count;
+  }
+  __syncthreads();
+  if (ea.hidden_out && ea.hidden) reorder_hidden(ea, s, s_count, s_pick);
+}
+
+// K5a alone, one warp per row over the whole GPU (4 rows per CTA).
+template <int KMAX>
+__global__ void __launch_bounds__(128) k_softmax_topb_warp(SoftmaxArgs sa) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (row >= sa.R_total) return;
+  const int s = row / sa.Bsent, i = row % sa.Bsent;
+  const bool live = !(sa.n_hyp && i >= sa.n_hyp[s]) && !(sa.finished && sa.finished[row]);
+  if (!live) {
+    if (lane == 0) sa.top_n[row] = 0;
+    return;
+  }
+  const uint32_t n = sa.n_cand[s];
+  float* L = sa.logits + static_cast<size_t>(row) * sa.ldl;
+  TopEntry* out = sa.top + static_cast<size_t>(row) * sa.topB;
+  if (n <= 32u * KMAX) fused_row_registers<KMAX>(sa, row, L, n, out, lane);
+  else fused_row_global(sa, row, L, n, out, lane);
+}
+
+lsb_status launch_softmax_warp(lsb_ctx* ctx, const SoftmaxArgs& sa, uint32_t max_n) {
+  const int grid = (sa.R_total + 3) / 4;
+  if (max_n <= 32u * 32u) k_softmax_topb_warp<32><<<grid, 128, 0, ctx->stream>>>(sa);
+  else k_softmax_topb_warp<48><<<grid, 128, 0, ctx->stream>>>(sa);
+  LSB_LAUNCHED(ctx, "k_softmax_topb_warp");
+  return LSB_OK;
+}
+
+// Fused K5 for the batched step: B <= 16 hypotheses per sentence. Rows up
+// to 32*KMAX candidates stay in registers (KMAX from the largest possible
+// row, ncap), longer ones take the global-memory path. `arrive` holds S
+// zeroed counters; the kernel leaves them zeroed.
+bool select_fused_applies(const SoftmaxArgs& sa, const ExpandArgs& ea) {
+  return sa.topB <= kFusedMaxB && sa.Bsent == sa.topB && !ea.frozen_mode && !ea.live_ids &&
+         !ea.id_map && !sa.probs_in && sa.n_cand;
+}
+
+lsb_status launch_select_fused(lsb_ctx* ctx, const SoftmaxArgs& sa, const ExpandArgs& ea,
+                               uint32_t max_n, uint32_t* arrive) {
+  (void)arrive;
+  const int S = sa.R_total / sa.Bsent;
+  const int threads = sa.Bsent * 32;
+  if (max_n <= 32u * 32u)
+    k_select_fused<32><<<S, threads, 0, ctx->stream>>>(sa, ea);
+  else
+    k_select_fused<48><<<S, threads, 0, ctx->stream>>>(sa, ea);
+  LSB_LAUNCHED(ctx, "k_select_fused");
+  return LSB_OK;
 }
 
 lsb_status launch_expand(lsb_ctx* ctx, const ExpandArgs& a) {

@@ -124,6 +124,12 @@ int tc_rows_per_tile(lsb_ctx* ctx, int rows, uint32_t ncols);
 constexpr int kTcMinRows = 64;  // rows sharing a column block before tensor cores pay
 lsb_status launch_softmax(lsb_ctx* ctx, const SoftmaxArgs& a);
 lsb_status launch_expand(lsb_ctx* ctx, const ExpandArgs& a);
+// Fused K5a+K5b (one launch; see k_select.cu) when select_fused_applies().
+bool select_fused_applies(const SoftmaxArgs& sa, const ExpandArgs& ea);
+// K5a with one warp per row (rows <= 32*48 candidates in registers).
+lsb_status launch_softmax_warp(lsb_ctx* ctx, const SoftmaxArgs& sa, uint32_t max_n);
+lsb_status launch_select_fused(lsb_ctx* ctx, const SoftmaxArgs& sa, const ExpandArgs& ea,
+                               uint32_t max_n, uint32_t* arrive);
 
 // Bitmap helpers for the stage API.
 lsb_status launch_bitmap_from_dense(lsb_ctx* ctx, const int32_t* L, int B, uint32_t V, int t,
