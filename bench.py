@@ -232,14 +232,20 @@ def run_ours(args, rank, world, local):
     logits_ms = float(stage_tot[2]) / max(nrec, 1)
     peak, peak_kind = measured_peak_hbm()
     achieved = alg_bytes / (logits_ms / 1e3) / 1e9
+    # The binding resource of K4 in PARITY is FP32 instruction issue, not HBM:
+    # every MAC is an FMUL + an FADD (no FMA, reference order). Peak lane-op
+    # rate = SMs x 128 FP32 lanes x SM clock (median under load).
+    macs = flops / 2.0
     roofline = {"kernel": "k_logits", "bound": "hbm", "achieved": round(achieved, 1),
                 "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": ncu_traffic(),
                 "alg_bytes_per_launch": int(alg_bytes), "launch_ms": round(logits_ms, 5),
                 "launches_timed": int(nrec),
+                "macs_per_launch": int(macs),
                 "fp32_tflops": round(flops / (logits_ms / 1e3) / 1e12, 2),
-                "note": "parity mode is FP32-issue bound (FMUL+FADD per MAC, no FMA)"
-                if mode == PARITY else "FFMA"}
+                "note": "PARITY: FP32-issue bound (FMUL+FADD per MAC in the reference order); "
+                        "see fp32_issue" if mode == PARITY else
+                        "FAST: top-T block on tcgen05 (3xTF32), survivors on FFMA"}
     stages = {k: round(float(v) / max(nrec, 1), 5) for k, v in
               zip(["probe_count", "compact", "logits", "softmax_topb", "expand"], stage_tot)}
 
@@ -294,6 +300,14 @@ def run_ours(args, rank, world, local):
                        "mean_vlsh": float(used.mean()), "index_build_ms": round(index_ms, 1)},
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
             "stage_ms": stages, "clocks": clk.summary(), **extras}
+    sm_mhz = line["clocks"].get("sm_mhz") or 1965.0
+    lane_ops = (2.0 if mode == PARITY else 1.0) * macs  # FMUL+FADD vs FFMA per MAC
+    peak_ops = ctx.sm_count * 128 * sm_mhz * 1e6
+    line["roofline"]["fp32_issue"] = {
+        "lane_ops_per_launch": int(lane_ops), "achieved_tops": round(lane_ops / (logits_ms / 1e3) / 1e12, 2),
+        "peak_tops": round(peak_ops / 1e12, 2), "frac": round(lane_ops / (logits_ms / 1e3) / peak_ops, 4),
+        "peak_basis": f"{ctx.sm_count} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (median SM clock "
+                      "in the timed region)"}
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(E, bias, H, scores, args.cpu_seconds)
     if world > 1:
@@ -339,7 +353,25 @@ def run_extras(ctx, model, idx, Hd, sc, fin, nh, choices, nchoice, hout, args, l
     ms = time_batch(b, 50)
     out["lsh_" + ("fast" if other == FAST else "parity")] = {
         "ms_per_step": round(ms, 4), "value": round(S / (ms / 1e3), 1)}
-    b.close()
+    # chosen-token agreement of FAST (tensor cores / FFMA) with PARITY on the
+    # same 50 step inputs: (beam, word) of every choice
+    bp = Batch(ctx, model, idx, S=S, B=B, T=c["T"], t=c["t"], specials=[c["V"] - 1], mode=PARITY)
+    bf = b if other == FAST else Batch(ctx, model, idx, S=S, B=B, T=c["T"], t=c["t"],
+                                       specials=[c["V"] - 1], mode=FAST)
+    agree = total = 0
+    for k in range(c["inputs"]):
+        got = []
+        for bb in (bp, bf):
+            bb.step(base + k * step_bytes, sc, fin, nh, choices, nchoice, hout)
+            ctx.sync()
+            got.append(choices.view(torch.int64).view(S, B, 3)[:, :, 1:].clone())
+        same = (got[0] == got[1]).all(dim=2)
+        agree += int(same.sum())
+        total += same.numel()
+    out["fast_vs_parity_choice_agreement"] = {"agree": agree, "total": total,
+                                              "frac": round(agree / max(total, 1), 6)}
+    for bb in {id(bp): bp, id(bf): bf, id(b): b}.values():
+        bb.close()
     return out
 
 

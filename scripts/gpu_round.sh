@@ -9,7 +9,7 @@ OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > "$OUT/gpu.txt" 2>&1
 lscpu > "$OUT/lscpu.txt" 2>&1
-timeout 1200 python -m pytest tests -m gpu -x -q > "$OUT/pytest_gpu.log" 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q --timeout 600 > "$OUT/pytest_gpu.log" 2>&1
 echo "pytest exit $?" >> "$OUT/pytest_gpu.log"
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1
 echo "smoke exit $?" >> "$OUT/smoke.log"
@@ -23,4 +23,10 @@ for k in $KERNELS; do
     -f -o "$OUT/prof_$k" python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-extras \
     > "$OUT/ncu_full_$k.log" 2>&1
 done
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_tc_logits" -s 5 -c 1 \
+  -f -o "$OUT/prof_k_tc_logits" python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-extras \
+  --mode fast > "$OUT/ncu_full_k_tc_logits.log" 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'^k_' -c 200 --csv \
+  --log-file "$OUT/launches_fast.csv" python bench.py --steps 20 --warmup 3 --no-cpu-baseline \
+  --no-extras --mode fast > "$OUT/ncu_launch_bench_fast.log" 2>&1
 echo done > "$OUT/DONE"
