@@ -183,6 +183,22 @@ class Context:
                 np.array([out[i].word for i in range(k)], np.int64))
 
 
+def exact_topb(ctx: "Context", model: "Model", H, rows: int, b: int, bias: bool = True):
+    """exact_topb_logits(H . E^T (+ bias), b) (src/eval_oracle.cpp:11-44) on the
+    device: per row the b largest full-vocabulary logits, ties to the smaller
+    id. ``H`` is a device pointer (int) or a host array. Returns (ids, values)."""
+    ids = np.zeros((rows, b), np.uint32)
+    vals = np.zeros((rows, b), np.float32)
+    if isinstance(H, int):
+        N.check(ctx.lib.lsb_exact_topb(ctx.h, model.h, H, rows, 1, b, int(bias), _p(ids),
+                                       _p(vals)), "exact_topb")
+    else:
+        Hh = _f32(H)
+        N.check(ctx.lib.lsb_exact_topb(ctx.h, model.h, _p(Hh), rows, 0, b, int(bias), _p(ids),
+                                       _p(vals)), "exact_topb")
+    return ids, vals
+
+
 class Model:
     """Device copy of E (|V| x d) and the logit bias (lsb_model)."""
 
