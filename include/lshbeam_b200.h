@@ -66,8 +66,10 @@ typedef struct lsb_batch lsb_batch; /* per-step scratch for S sentences   */
 /* ------------------------------------------------------------ 1. context */
 const char* lsb_last_error(void);
 int lsb_abi_version(void);
-/* stream: a cudaStream_t on `device`, or NULL to create a private
- * non-blocking stream. */
+/* stream: a cudaStream_t on `device`, LSB_STREAM_LEGACY for the legacy
+ * default stream (cudaStreamLegacy), or NULL to create a private
+ * non-blocking stream (which does NOT synchronise with the default stream). */
+#define LSB_STREAM_LEGACY ((void*)0x1)
 lsb_status lsb_ctx_create(int device, void* stream, lsb_ctx** out);
 lsb_status lsb_ctx_destroy(lsb_ctx* ctx);
 lsb_status lsb_ctx_sync(lsb_ctx* ctx);       /* sync + surface device errors */

@@ -13,6 +13,7 @@ LIB_PATH = os.path.join(PKG, "liblshbeam_b200.so")
 
 LSB_OK, LSB_EINVAL, LSB_ERUNTIME, LSB_ECUDA, LSB_ENOMEM = range(5)
 MODE_PARITY, MODE_FAST = 0, 1
+STREAM_LEGACY = 1  # LSB_STREAM_LEGACY: cudaStreamLegacy, the legacy default stream
 
 
 class lsb_choice(C.Structure):

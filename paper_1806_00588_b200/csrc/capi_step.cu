@@ -167,6 +167,8 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
   if (e == cudaSuccess && !spec.empty())
     e = cudaMemcpy(b->specials, spec.data(), spec.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = dalloc(&b->qcodes, SB * (b->idx ? b->idx->W : 1));
+  // rows that are frozen or past n_hyp are never hashed; keep their codes defined
+  if (e == cudaSuccess) e = cudaMemset(b->qcodes, 0, SB * (b->idx ? b->idx->W : 1) * 4);
   if (e == cudaSuccess) e = dalloc(&b->bitmap, static_cast<size_t>(b->S) * b->nwords);
   if (e == cudaSuccess)
     e = cudaMemset(b->bitmap, 0, std::max<size_t>(1, static_cast<size_t>(b->S) * b->nwords) * 4);

@@ -85,6 +85,40 @@ __device__ __forceinline__ void mac4(float (&acc)[RB][CB][PARITY ? 4 : 1], const
   }
 }
 
+// PARITY with Blackwell's paired FP32 pipe (FFMA2 on f32x2 register pairs):
+// lanes (0,1) and (2,3) of the reference's 4-lane accumulation advance
+// together. Exactness: fma(h, e, -0) == fl(h*e) and fma(acc, 1, p) ==
+// fl(acc + p) (a single rounding each, the same signed zeros), so the pair
+// ops reproduce FMUL/FADD bit for bit. The -0 / 1.0 operands come from
+// kernel arguments: were they compile-time constants, ptxas would turn the
+// pair back into mul + add and contract it into one FFMA2, which rounds once
+// instead of twice.
+__device__ __forceinline__ unsigned long long f2fma(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+template <int RB, int CB>
+__device__ __forceinline__ void mac4_x2(unsigned long long (&acc)[RB][CB][2], const float* Es,
+                                        const float* Hs, int tid, int k4,
+                                        unsigned long long negz, unsigned long long one) {
+  ulonglong2 e[CB];
+#pragma unroll
+  for (int cb = 0; cb < CB; ++cb)
+    e[cb] = *reinterpret_cast<const ulonglong2*>(Es + (tid + cb * kLT) * kKS + k4 * 4);
+#pragma unroll
+  for (int rb = 0; rb < RB; ++rb) {
+    const ulonglong2 h = *reinterpret_cast<const ulonglong2*>(Hs + rb * kKS + k4 * 4);
+#pragma unroll
+    for (int cb = 0; cb < CB; ++cb) {
+      acc[rb][cb][0] = f2fma(acc[rb][cb][0], one, f2fma(h.x, e[cb].x, negz));
+      acc[rb][cb][1] = f2fma(acc[rb][cb][1], one, f2fma(h.y, e[cb].y, negz));
+    }
+  }
+}
+
 template <int RB, int CB, bool PARITY, bool VEC, int kStages>
 __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs a) {
   extern __shared__ __align__(16) float sm[];
@@ -185,6 +219,14 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
       for (int cb = 0; cb < CB; ++cb)
 #pragma unroll
         for (int k = 0; k < NA; ++k) acc[rb][cb][k] = 0.0f;
+    constexpr bool X2 = PARITY && VEC;  // paired FP32 path (see mac4_x2)
+    unsigned long long acc2[X2 ? RB : 1][X2 ? CB : 1][2];
+    if constexpr (X2) {
+#pragma unroll
+      for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb) acc2[rb][cb][0] = acc2[rb][cb][1] = 0ull;
+    }
 
 #pragma unroll
     for (int st = 0; st < kStages - 1; ++st) {
@@ -205,15 +247,44 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
       const float* Hs = Es + CT * kKS;
       const int kv = max(0, min(kKC, d4 - kc * kKC)) >> 2;  // full 4-lane groups
       if (warp_live) {
-        if (kv == kKC / 4) {
+        bool done = false;
+        if constexpr (X2) {
+          if (a.use_x2) {
+            done = true;
+            if (kv == kKC / 4) {
 #pragma unroll
-          for (int k4 = 0; k4 < kKC / 4; ++k4) mac4<RB, CB, PARITY>(acc, Es, Hs, tid, k4);
-        } else {
-          for (int k4 = 0; k4 < kv; ++k4) mac4<RB, CB, PARITY>(acc, Es, Hs, tid, k4);
+            for (int k4 = 0; k4 < kKC / 4; ++k4)
+                mac4_x2<RB, CB>(acc2, Es, Hs, tid, k4, a.x2_negzero, a.x2_one);
+            } else {
+              for (int k4 = 0; k4 < kv; ++k4)
+                mac4_x2<RB, CB>(acc2, Es, Hs, tid, k4, a.x2_negzero, a.x2_one);
+            }
+          }
+        }
+        if (!done) {
+          if (kv == kKC / 4) {
+#pragma unroll
+            for (int k4 = 0; k4 < kKC / 4; ++k4) mac4<RB, CB, PARITY>(acc, Es, Hs, tid, k4);
+          } else {
+            for (int k4 = 0; k4 < kv; ++k4) mac4<RB, CB, PARITY>(acc, Es, Hs, tid, k4);
+          }
         }
       }
     }
     cp_async_wait<0>();
+    if constexpr (X2) {
+      if (a.use_x2) {  // unpack the pairs into the four reference lanes
+#pragma unroll
+      for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb) {
+          acc[rb][cb][0] = __uint_as_float(static_cast<uint32_t>(acc2[rb][cb][0]));
+          acc[rb][cb][1] = __uint_as_float(static_cast<uint32_t>(acc2[rb][cb][0] >> 32));
+          acc[rb][cb][2] = __uint_as_float(static_cast<uint32_t>(acc2[rb][cb][1]));
+          acc[rb][cb][3] = __uint_as_float(static_cast<uint32_t>(acc2[rb][cb][1] >> 32));
+        }
+      }
+    }
     // the d mod 4 tail (all of d when d < 4) sits in the last chunk: lane 0
     if (d4 < d && warp_live) {
       const int cl = (nchunks - 1) * kKC;
@@ -321,6 +392,10 @@ static lsb_status launch_logits_rb(lsb_ctx* ctx, LogitsArgs a, int target) {
 // (FAST) per 16-byte E load; 5 CTAs per SM.
 lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_ctas) {
   const bool fast = mode == LSB_MODE_FAST;
+  a.x2_negzero = 0x8000000080000000ull;  // runtime operands of the paired FP32 path
+  a.x2_one = 0x3F8000003F800000ull;
+  static const bool no_x2 = getenv("LSB_NO_X2") != nullptr;
+  a.use_x2 = no_x2 ? 0 : 1;
   // FAST + enough rows sharing the identity columns [0, n_shared): a dense
   // contraction -> tcgen05 tensor cores; the per-sentence survivors stay on
   // the FFMA kernel below.

@@ -52,6 +52,12 @@ class Context:
     def __init__(self, device: int = 0, stream: int | None = None):
         self.lib = N.load()
         h = C.c_void_p()
+        # torch reports its default (legacy NULL) stream as handle 0; the C ABI
+        # reads NULL as "create a private stream", so map 0 to cudaStreamLegacy
+        # (LSB_STREAM_LEGACY) -- otherwise work queued by torch on the default
+        # stream would not be ordered with ours.
+        if stream == 0:
+            stream = N.STREAM_LEGACY
         N.check(self.lib.lsb_ctx_create(device, stream, C.byref(h)), "lsb_ctx_create")
         self.h = h
         self.device = device
