@@ -167,13 +167,13 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
     // piece i covers column (tid >> 3) + 16 i, floats [4 (tid & 7), +4) of
     // every chunk; invalid columns / rows carry bit 31 and are zero-filled
     const int part = tid & 7;
-    uint32_t eoff[VEC ? 8 * CB : 1];
+    // sid[] now holds each column's element offset sid*d (bit 31 = invalid),
+    // re-read per chunk instead of pinning 8 registers per thread
     if constexpr (VEC) {
-#pragma unroll
-      for (int i = 0; i < 8 * CB; ++i) {
-        const int col = (tid >> 3) + 16 * i;
-        eoff[i] = col < ncols ? sid[col] * static_cast<uint32_t>(d) + part * 4 : 0x80000000u;
-      }
+      __syncthreads();
+      for (int c = tid; c < CT; c += kLT)
+        sid[c] = c < ncols ? sid[c] * static_cast<uint32_t>(d) : 0x80000000u;
+      __syncthreads();
     }
     const int hrow = tid >> 3;
     const uint32_t hoff = (tid < RB * 8 && row0 + hrow < rowlim)
@@ -188,9 +188,10 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
         const bool kin = c0 + part * 4 < d;
 #pragma unroll
         for (int i = 0; i < 8 * CB; ++i) {
-          const bool ok = kin && !(eoff[i] & 0x80000000u);
-          cp_async16(Es + ((tid >> 3) + 16 * i) * kKS + part * 4, a.E + (ok ? eoff[i] + c0 : 0),
-                     ok ? 16 : 0);
+          const uint32_t off = sid[(tid >> 3) + 16 * i];
+          const bool ok = kin && !(off & 0x80000000u);
+          cp_async16(Es + ((tid >> 3) + 16 * i) * kKS + part * 4,
+                     a.E + (ok ? off + part * 4 + c0 : 0), ok ? 16 : 0);
         }
         if (tid < RB * 8) {
           const bool ok = kin && !(hoff & 0x80000000u);
@@ -307,7 +308,8 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
     for (int cb = 0; cb < CB; ++cb) {
       const int c = tid + kLT * cb;
       if (c >= ncols) continue;
-      const float bias = a.bias ? __ldg(a.bias + sid[c]) : 0.0f;
+      const uint32_t wid = VEC ? sid[c] / static_cast<uint32_t>(d) : sid[c];  // VEC: sid = id*d
+      const float bias = a.bias ? __ldg(a.bias + wid) : 0.0f;
       const size_t col = col0 + c;
 #pragma unroll
       for (int rb = 0; rb < RB; ++rb) {

@@ -47,6 +47,109 @@ __device__ __forceinline__ T block_reduce(T v, T* red, Op op) {
   return v;
 }
 
+// Rows of at most kSelT * kSelReg candidates (the LSH step's): the row lives
+// in registers, kSelReg values per thread -- one global read, no exp/prob
+// round trips through L2 -- and the top-B is B rounds of a block-wide
+// arg-max by (p desc, column asc) in which only the owner of the winning
+// column rescans its registers. Same arithmetic as the general path.
+constexpr int kSelReg = 16;
+
+__device__ __forceinline__ void row_registers(const SoftmaxArgs& a, int row, float* L, uint32_t n,
+                                              float* red_f, double* red_d) {
+  __shared__ float win_p[2][kSelT / 32];
+  __shared__ uint32_t win_r[2][kSelT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int B = a.topB;
+  float v[kSelReg];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < kSelReg; ++k) {
+    const uint32_t c = tid + kSelT * k;
+    v[k] = c < n ? L[c] : -INFINITY;
+    mx = (mx < v[k]) ? v[k] : mx;
+  }
+  mx = block_reduce(mx, red_f, [](float x, float y) { return (x < y) ? y : x; });
+  if (n == 0 || (isinf(mx) && mx < 0)) {
+    if (tid == 0) {
+      atomicOr(a.err, kErrEmptyRow);
+      a.top_n[row] = 0;
+    }
+    return;
+  }
+  const double dmx = static_cast<double>(mx);
+  double sum = 0.0;
+#pragma unroll
+  for (int k = 0; k < kSelReg; ++k) {
+    if (tid + kSelT * k < n) {
+      const double e = exp(static_cast<double>(v[k]) - dmx);
+      v[k] = static_cast<float>(e);
+      sum += e;
+    }
+  }
+  sum = block_reduce(sum, red_d, [](double x, double y) { return x + y; });
+  const float inv = static_cast<float>(1.0 / sum);
+#pragma unroll
+  for (int k = 0; k < kSelReg; ++k) {
+    const uint32_t c = tid + kSelT * k;
+    if (c < n) {
+      v[k] = __fmul_rn(v[k], inv);
+      if (a.keep_probs) L[c] = v[k];
+    } else {
+      v[k] = -1.0f;
+    }
+  }
+  float bp = -1.0f;
+  int bk = 0;
+#pragma unroll
+  for (int k = 0; k < kSelReg; ++k)
+    if (v[k] > bp) {
+      bp = v[k];
+      bk = k;
+    }
+  TopEntry* out = a.top + static_cast<size_t>(row) * B;
+  const int keep = static_cast<int>(min(static_cast<uint32_t>(B), n));
+  for (int r = 0; r < keep; ++r) {
+    float p = bp;
+    uint32_t c = bp >= 0.0f ? tid + kSelT * static_cast<uint32_t>(bk) : 0xFFFFFFFFu;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float yp = __shfl_xor_sync(0xffffffffu, p, o);
+      const uint32_t yc = __shfl_xor_sync(0xffffffffu, c, o);
+      if (top_better(yp, yc, p, c)) {
+        p = yp;
+        c = yc;
+      }
+    }
+    const int buf = r & 1;  // double-buffered winners: one barrier per round
+    if (lane == 0) {
+      win_p[buf][warp] = p;
+      win_r[buf][warp] = c;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kSelT / 32; ++w)
+      if (top_better(win_p[buf][w], win_r[buf][w], p, c)) {
+        p = win_p[buf][w];
+        c = win_r[buf][w];
+      }
+    if (tid == 0) out[r] = TopEntry{p, c};
+    if (c % kSelT == static_cast<uint32_t>(tid)) {  // the owner drops it and rescans
+#pragma unroll
+      for (int k = 0; k < kSelReg; ++k)
+        if (k == bk) v[k] = -1.0f;
+      bp = -1.0f;
+      bk = 0;
+#pragma unroll
+      for (int k = 0; k < kSelReg; ++k)
+        if (v[k] > bp) {
+          bp = v[k];
+          bk = k;
+        }
+    }
+  }
+  if (tid == 0) a.top_n[row] = keep;
+}
+
 // ===================================================================== K5a
 __global__ void __launch_bounds__(kSelT) k_softmax_topb(SoftmaxArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -65,6 +168,10 @@ __global__ void __launch_bounds__(kSelT) k_softmax_topb(SoftmaxArgs a) {
   const int B = a.topB;
   const uint32_t n = a.n_cand ? a.n_cand[s] : a.n_const;
   float* L = a.logits + static_cast<size_t>(row) * a.ldl;
+  if (!a.probs_in && n <= kSelT * kSelReg && B > 0) {
+    row_registers(a, row, L, n, red_f, red_d);
+    return;
+  }
   float inv = 1.0f;
   if (!a.probs_in) {
     // float max, as std::max over the row (src/beam_decoder.cpp:55)

@@ -1,0 +1,6 @@
+#!/bin/bash
+mkdir -p gpurun_out/ab
+timeout 300 python -m pytest tests/test_gpu_step.py tests/test_gpu_stages.py -x -q --timeout 200 > gpurun_out/ab/pytest.log 2>&1; echo "exit $?" >> gpurun_out/ab/pytest.log
+for rep in 1 2; do
+  timeout 300 python bench.py --no-cpu-baseline --no-extras --steps 300 > gpurun_out/ab/base_$rep.json 2>/dev/null
+done
