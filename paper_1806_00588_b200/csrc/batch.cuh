@@ -19,6 +19,7 @@ struct lsb_batch {
   size_t ncap = 0;
   uint32_t nwords = 0, slice_len = 0;
   int counter_bytes = 1;
+  int levels = -1;  // bit-sliced hit counting when 1 <= t <= 8
   int nspec = 0;
   int keep_probs = 0;
   // device scratch

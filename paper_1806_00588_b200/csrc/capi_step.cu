@@ -62,6 +62,7 @@ lsb_status lsb::step_front(lsb_batch* b, const lsb_state_dev* in, int empty_is_e
     pa.t = b->t;
     pa.slice_len = b->slice_len;
     pa.counter_bytes = b->counter_bytes;
+    pa.levels = b->levels;
     pa.qcodes = b->qcodes;
     pa.bitmap = b->bitmap;
     pa.nwords = b->nwords;
@@ -158,9 +159,17 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
   b->nspec = static_cast<int>(spec.size());
   if (b->idx) {
     b->counter_bytes = b->idx->W < 256 ? 1 : 2;
-    const uint32_t budget = 96 * 1024 / b->counter_bytes;
-    const uint32_t nslices = (V + budget - 1) / budget;
-    b->slice_len = ((V + nslices - 1) / nslices + 63) & ~63u;
+    if (b->t >= 1 && b->t <= 8) {
+      // t bit planes of the slice (t-1 levels + the marked set), <= 32 KB
+      b->levels = b->t - 1;
+      const uint32_t budget = 32 * 1024 * 8 / b->t;  // words per slice
+      const uint32_t nslices = (V + budget - 1) / budget;
+      b->slice_len = ((V + nslices - 1) / nslices + 127) & ~127u;  // planes of 16-B multiples
+    } else {
+      const uint32_t budget = 96 * 1024 / b->counter_bytes;
+      const uint32_t nslices = (V + budget - 1) / budget;
+      b->slice_len = ((V + nslices - 1) / nslices + 63) & ~63u;
+    }
   }
   const size_t SB = static_cast<size_t>(b->S) * b->B;
   cudaError_t e = dalloc(&b->specials, spec.size());

@@ -32,7 +32,11 @@ __global__ void __launch_bounds__(512) k_probe_count(ProbeArgs a) {
   const uint32_t lo = blockIdx.y * a.slice_len;
   const uint32_t hi = min(ix.V, lo + a.slice_len);
   const bool count = a.t > 0;
-  const size_t cbytes = count ? ((static_cast<size_t>(a.slice_len) * a.counter_bytes + 15) & ~size_t(15)) : 0;
+  const bool bits = a.levels >= 0;  // bit-sliced counting (t <= 8)
+  const size_t cbytes =
+      !count ? 0
+      : bits ? static_cast<size_t>(a.levels + 1) * (a.slice_len / 8)
+             : ((static_cast<size_t>(a.slice_len) * a.counter_bytes + 15) & ~size_t(15));
   uint32_t* cnt = reinterpret_cast<uint32_t*>(smem);
   float* h = reinterpret_cast<float*>(smem + cbytes);
   const int dpad = (ix.d + 3) & ~3;
@@ -41,6 +45,15 @@ __global__ void __launch_bounds__(512) k_probe_count(ProbeArgs a) {
 
   for (size_t k = threadIdx.x; k < cbytes / 16; k += blockDim.x)
     reinterpret_cast<uint4*>(cnt)[k] = make_uint4(0, 0, 0, 0);
+  // this thread's permutation row, fetched while the hidden row is in flight
+  constexpr int kMaxKReg = 16;
+  uint32_t pk[kMaxKReg];
+  const int p_own = threadIdx.x;
+  if (p_own < ix.P && ix.K <= kMaxKReg) {
+    const uint32_t* pr = ix.perms + static_cast<size_t>(p_own) * ix.K;
+#pragma unroll
+    for (int k = 0; k < kMaxKReg; ++k) pk[k] = k < ix.K ? __ldg(pr + k) : 0u;
+  }
   const float* src = a.hidden + static_cast<size_t>(row) * ix.d;
   int nan = 0;
   if ((ix.d & 3) == 0) {
@@ -61,6 +74,23 @@ __global__ void __launch_bounds__(512) k_probe_count(ProbeArgs a) {
     return;
   }
   // K1: windowed argmax per permutation, ties to the smallest k.
+  if (ix.K <= kMaxKReg && ix.P <= static_cast<int>(blockDim.x)) {
+    if (p_own < ix.P) {
+      uint32_t best = 0;
+      float bv = h[pk[0]];
+#pragma unroll
+      for (int k = 1; k < kMaxKReg; ++k) {
+        if (k < ix.K) {
+          const float v = h[pk[k]];
+          if (v > bv) {
+            bv = v;
+            best = k;
+          }
+        }
+      }
+      idx[p_own] = static_cast<uint8_t>(best);
+    }
+  } else
   for (int p = threadIdx.x; p < ix.P; p += blockDim.x) {
     const uint32_t* pr = ix.perms + static_cast<size_t>(p) * ix.K;
     uint32_t best = 0;
@@ -90,10 +120,28 @@ __global__ void __launch_bounds__(512) k_probe_count(ProbeArgs a) {
     uint32_t start, len;
     if (!warp_probe(ix, w, codes[w], start, len)) continue;
     const uint32_t* ids = ix.word_ids + static_cast<size_t>(w) * ix.V + start;
-    for (uint32_t k = lane; k < len; k += 32) {
-      const uint32_t id = __ldg(ids + k);
+    // 4 independent loads per lane in flight before the shared-memory updates
+    constexpr int U = 4;
+    for (uint32_t k0 = lane; k0 < len; k0 += 32 * U) {
+    uint32_t idu[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) idu[u] = k0 + 32 * u < len ? __ldg(ids + k0 + 32 * u) : 0xFFFFFFFFu;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t id = idu[u];
       if (id < lo || id >= hi) continue;
       const uint32_t local = id - lo;
+      if (bits) {
+        // level k holds "seen more than k times"; a visit climbs one level,
+        // the one after level t-2 marks the word (count == t)
+        const uint32_t wd = local >> 5, bit = 1u << (local & 31);
+        const uint32_t nw = a.slice_len >> 5;
+        int lvl = 0;
+        for (; lvl < a.levels; ++lvl)
+          if (!(atomicOr(cnt + lvl * nw + wd, bit) & bit)) break;
+        if (lvl == a.levels) atomicOr(cnt + a.levels * nw + wd, bit);
+        continue;
+      }
       uint32_t c;
       if (a.counter_bytes == 1) {
         const uint32_t sh = (local & 3) * 8;
@@ -104,6 +152,15 @@ __global__ void __launch_bounds__(512) k_probe_count(ProbeArgs a) {
       }
       if (c + 1 == t) atomicOr(bm + (id >> 5), 1u << (id & 31));
     }
+    }
+  }
+  if (bits) {  // OR this slice's marked words into the sentence bitmap
+    __syncthreads();
+    const uint32_t nw = a.slice_len >> 5;
+    const uint32_t* fin = cnt + a.levels * nw;
+    const uint32_t w0 = lo >> 5, wend = min(nw, a.nwords - w0);
+    for (uint32_t w = threadIdx.x; w < wend; w += blockDim.x)
+      if (fin[w]) atomicOr(bm + w0 + w, fin[w]);
   }
 }
 
@@ -111,7 +168,9 @@ lsb_status launch_probe(lsb_ctx* ctx, const ProbeArgs& a) {
   const IndexView& ix = a.ix;
   const uint32_t nslices = a.t > 0 ? (ix.V + a.slice_len - 1) / a.slice_len : 1;
   const size_t cbytes =
-      a.t > 0 ? ((static_cast<size_t>(a.slice_len) * a.counter_bytes + 15) & ~size_t(15)) : 0;
+      a.t <= 0 ? 0
+      : a.levels >= 0 ? static_cast<size_t>(a.levels + 1) * (a.slice_len / 8)
+                      : ((static_cast<size_t>(a.slice_len) * a.counter_bytes + 15) & ~size_t(15));
   const size_t smem = cbytes + ((ix.d + 3) & ~3) * 4 + ix.W * 4 + ix.P + 16;
   if (smem > ctx->smem_optin) {
     set_error("probe: shared memory budget exceeded");
@@ -124,7 +183,9 @@ lsb_status launch_probe(lsb_ctx* ctx, const ProbeArgs& a) {
     configured = smem;
   }
   dim3 grid(a.S * a.B, std::max(1u, nslices));
-  k_probe_count<<<grid, 512, smem, ctx->stream>>>(a);
+  // bit-sliced counters need little shared memory: 256-thread CTAs, 8 per SM,
+  // so a 768-row step runs in one wave
+  k_probe_count<<<grid, a.levels >= 0 ? 256 : 512, smem, ctx->stream>>>(a);
   LSB_LAUNCHED(ctx, "k_probe_count");
   return LSB_OK;
 }

@@ -19,7 +19,8 @@ struct ProbeArgs {
   const int32_t* n_hyp;     // [S] or null (all B)
   int S, B, t;
   uint32_t slice_len;       // counters per CTA (multiple of 64)
-  int counter_bytes;        // 1 or 2
+  int counter_bytes;        // 1 or 2 (byte counters)
+  int levels;               // >= 0: bit-sliced counting with t-1 levels (t <= 8); -1: counters
   uint32_t* qcodes;         // [S*B][W]
   uint32_t* bitmap;         // [S][nwords]
   uint32_t nwords;
