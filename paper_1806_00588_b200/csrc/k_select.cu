@@ -345,7 +345,7 @@ __device__ void reorder_hidden(const ExpandArgs& a, int s, int count, const uint
 // Rank selection. Lists: [0, nfz) explicit frozen singletons, then one list
 // per hypothesis row (a finished row is a singleton carrying its score).
 // Shared memory: per list off/len (ints), then per candidate score, beam, word.
-constexpr int kExpT = 256;
+constexpr int kExpT = 512;
 constexpr int kRankMaxLists = 128;
 
 __global__ void __launch_bounds__(kExpT) k_expand(ExpandArgs a) {
@@ -364,6 +364,8 @@ __global__ void __launch_bounds__(kExpT) k_expand(ExpandArgs a) {
   double* cs = reinterpret_cast<double*>(smem);
   long long* cw = reinterpret_cast<long long*>(cs + cap);
   uint32_t* cb = reinterpret_cast<uint32_t*>(cw + cap);
+  int* co = reinterpret_cast<int*>(cb + cap);  // own list of each candidate
+  int* cr = co + cap;                          // rank accumulators
 
   // list lengths -> offsets (nl <= kRankMaxLists: one warp scans)
   if (threadIdx.x < 32) {
@@ -423,30 +425,29 @@ __global__ void __launch_bounds__(kExpT) k_expand(ExpandArgs a) {
     cs[e] = sc;
     cb[e] = beam;
     cw[e] = wd;
+    co[e] = l;
+    cr[e] = j;  // position in its own list
   }
   __syncthreads();
-  // rank = own position + per other list the count of better entries
+  // rank = own position + per other list the count of better entries; one
+  // (candidate, list) pair per thread so the binary searches run in parallel
   const int B = a.topB;
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {
-    int lo = 0, hi = nl - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_off[mid] <= e) lo = mid;
-      else hi = mid - 1;
-    }
-    const int own = lo;
+  for (int q = threadIdx.x; q < total * nl; q += blockDim.x) {
+    const int e = q / nl, l = q - e * nl;
+    if (l == co[e] || s_off[l] == s_off[l + 1]) continue;
     const Cand me{cs[e], cb[e], cw[e]};
-    int rank = e - s_off[own];
-    for (int l = 0; l < nl && rank < B; ++l) {
-      if (l == own) continue;
-      int b0 = s_off[l], b1 = s_off[l + 1];  // first entry of l not better than me
-      while (b0 < b1) {
-        const int mid = (b0 + b1) >> 1;
-        if (cand_better(Cand{cs[mid], cb[mid], cw[mid]}, me)) b0 = mid + 1;
-        else b1 = mid;
-      }
-      rank += b0 - s_off[l];
+    int b0 = s_off[l], b1 = s_off[l + 1];  // first entry of l not better than me
+    while (b0 < b1) {
+      const int mid = (b0 + b1) >> 1;
+      if (cand_better(Cand{cs[mid], cb[mid], cw[mid]}, me)) b0 = mid + 1;
+      else b1 = mid;
     }
+    if (b0 > s_off[l]) atomicAdd(cr + e, b0 - s_off[l]);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int rank = cr[e];
+    const Cand me{cs[e], cb[e], cw[e]};
     if (rank < B) {
       a.choices[static_cast<size_t>(s) * B + rank] =
           lsb_choice{me.score, me.beam, 0u, static_cast<int64_t>(me.word)};
@@ -873,7 +874,7 @@ lsb_status launch_select_fused(lsb_ctx* ctx, const SoftmaxArgs& sa, const Expand
 lsb_status launch_expand(lsb_ctx* ctx, const ExpandArgs& a) {
   if (a.S == 0) return LSB_OK;
   const int nl = (a.frozen_mode ? a.nfrozen : 0) + a.Bsent;
-  const size_t rank_smem = static_cast<size_t>(nl) * std::max(a.topB, 1) * (8 + 8 + 4);
+  const size_t rank_smem = static_cast<size_t>(nl) * std::max(a.topB, 1) * (8 + 8 + 4 + 4 + 4);
   if (nl <= kRankMaxLists && rank_smem <= ctx->smem_optin) {
     static size_t configured = 0;
     if (rank_smem > configured) {
@@ -881,7 +882,7 @@ lsb_status launch_expand(lsb_ctx* ctx, const ExpandArgs& a) {
                                     static_cast<int>(rank_smem)));
       configured = rank_smem;
     }
-    k_expand<<<a.S, kExpT, rank_smem, ctx->stream>>>(a);
+    k_expand<<<a.S, kExpT, rank_smem, ctx->stream>>>(a);  // kExpT threads per sentence
     LSB_LAUNCHED(ctx, "k_expand");
     return LSB_OK;
   }
