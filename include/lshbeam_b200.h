@@ -250,7 +250,8 @@ const uint32_t* lsb_batch_n_cand_dev(lsb_batch* b);
 lsb_status lsb_batch_keep_probs(lsb_batch* b, int on);
 
 /* Per-kernel device time, milliseconds, measured with CUDA events recorded
- * on the context stream between the step's kernels when profiling is on:
+ * on the context stream between the step's kernels when profiling is on
+ * (lsb_batch_profile(b, n): n = 1 every step, n > 1 every n-th step, 0 off):
  * [probe_count, compact, logits, softmax_topb, expand]. stage_ms: last step;
  * stage_totals: sum over the steps since the previous call (<= 1024). */
 lsb_status lsb_batch_profile(lsb_batch* b, int on);

@@ -51,6 +51,9 @@ struct lsb_batch {
   bool has_last = false;
   // profiling: one set of 6 events per step in a ring, summed on demand
   bool profile = false;
+  int profile_every = 1;   // record stage events on every n-th step
+  uint64_t step_count = 0;
+  bool rec = false;        // this step records stage events
   std::vector<cudaEvent_t> ring;  // kRing * 6
   int ring_next = 0, ring_used = 0;
   cudaEvent_t* ev = nullptr;       // current step's 6 events

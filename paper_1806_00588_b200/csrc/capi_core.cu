@@ -3,6 +3,8 @@
 #include <cstring>
 #include <string>
 
+#include <cstdlib>
+
 #include "lsb_internal.cuh"
 
 namespace lsb {
@@ -38,6 +40,7 @@ lsb_status lsb_ctx_create(int device, void* stream, lsb_ctx** out) {
     return LSB_EINVAL;
   }
   LSB_CUDA(cudaSetDevice(device));
+  const bool pdl = getenv("LSB_NO_PDL") == nullptr;  // A/B switch for measurements
   cudaDeviceProp prop;
   LSB_CUDA(cudaGetDeviceProperties(&prop, device));
   if (prop.major != 10) {
@@ -46,6 +49,7 @@ lsb_status lsb_ctx_create(int device, void* stream, lsb_ctx** out) {
     return LSB_ECUDA;
   }
   auto* c = new lsb_ctx;
+  c->pdl = pdl ? 1 : 0;
   c->device = device;
   c->sm_count = prop.multiProcessorCount;
   c->smem_optin = prop.sharedMemPerBlockOptin;

@@ -44,7 +44,8 @@ lsb_status lsb::step_front(lsb_batch* b, const lsb_state_dev* in, int empty_is_e
   cudaStream_t st = ctx->stream;
   const int R = b->S * b->B;
   lsb_status rc;
-  if (b->profile) {
+  b->rec = b->profile && (b->step_count++ % static_cast<uint64_t>(b->profile_every)) == 0;
+  if (b->rec) {
     b->ev = &b->ring[static_cast<size_t>(b->ring_next) * 6];
     b->ring_next = (b->ring_next + 1) % kRing;
     b->ring_used = std::min(b->ring_used + 1, kRing);
@@ -69,7 +70,7 @@ lsb_status lsb::step_front(lsb_batch* b, const lsb_state_dev* in, int empty_is_e
     pa.err = ctx->err_dev;
     if ((rc = launch_probe(ctx, pa))) return rc;
   }
-  if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[1], st));
+  if (b->rec) LSB_CUDA(cudaEventRecord(b->ev[1], st));
   // K3
   CompactArgs ca{};
   ca.bitmap_in = b->bitmap;
@@ -90,7 +91,7 @@ lsb_status lsb::step_front(lsb_batch* b, const lsb_state_dev* in, int empty_is_e
   ca.B = b->B;
   ca.err = ctx->err_dev;
   if ((rc = launch_compact(ctx, ca, b->S))) return rc;
-  if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[2], st));
+  if (b->rec) LSB_CUDA(cudaEventRecord(b->ev[2], st));
   // K4
   LogitsArgs la{};
   la.H = in->hidden;
@@ -110,7 +111,7 @@ lsb_status lsb::step_front(lsb_batch* b, const lsb_state_dev* in, int empty_is_e
   la.tc_H = b->tc_H;
   la.tc_N = b->tc_N;
   if ((rc = launch_logits(ctx, la, b->mode, ctx->sm_count * 8))) return rc;
-  if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[3], st));
+  if (b->rec) LSB_CUDA(cudaEventRecord(b->ev[3], st));
   return LSB_OK;
 }
 
@@ -222,6 +223,10 @@ lsb_status lsb_batch_keep_probs(lsb_batch* b, int on) {
 
 lsb_status lsb_batch_profile(lsb_batch* b, int on) {
   if (!b) return LSB_EINVAL;
+  // on > 1: sample every on-th step (stage events break programmatic
+  // dependent launch between the kernels they separate)
+  b->profile_every = on > 1 ? on : 1;
+  b->step_count = 0;
   if (on && b->ring.empty()) {
     b->ring.assign(kRing * 6, nullptr);
     for (auto& e : b->ring) LSB_CUDA(cudaEventCreate(&e));
@@ -312,18 +317,18 @@ lsb_status lsb_step(lsb_batch* b, const lsb_state_dev* in, const lsb_out_dev* ou
   if (b->cmode == 0 && k5 == 2 && select_fused_applies(sa, ea)) {
     // one launch: CTA per sentence, warp per row, then the expansion
     if ((rc = launch_select_fused(ctx, sa, ea, static_cast<uint32_t>(b->ncap), b->arrive))) return rc;
-    if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[4], st));
+    if (b->rec) LSB_CUDA(cudaEventRecord(b->ev[4], st));
   } else if (b->cmode == 0 && k5 == 1) {
     // warp per row over the whole GPU, then the per-sentence expansion
     if ((rc = launch_softmax_warp(ctx, sa, static_cast<uint32_t>(b->ncap)))) return rc;
-    if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[4], st));
+    if (b->rec) LSB_CUDA(cudaEventRecord(b->ev[4], st));
     if ((rc = launch_expand(ctx, ea))) return rc;
   } else {
     if ((rc = launch_softmax(ctx, sa))) return rc;
-    if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[4], st));
+    if (b->rec) LSB_CUDA(cudaEventRecord(b->ev[4], st));
     if ((rc = launch_expand(ctx, ea))) return rc;
   }
-  if (b->profile) LSB_CUDA(cudaEventRecord(b->ev[5], st));
+  if (b->rec) LSB_CUDA(cudaEventRecord(b->ev[5], st));
   b->last = *in;
   b->has_last = true;
   return LSB_OK;

@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
   const int d4 = d & ~3;
   const int nchunks = (d + kKC - 1) / kKC;
 
+  pdl_wait();
   const bool shared_job = static_cast<int>(blockIdx.x) < a.jobs_shared;
   int row0, rowlim, tile_first, tile_step, s = 0;
   uint32_t m = 0;
@@ -358,7 +359,7 @@ static lsb_status launch_variant(lsb_ctx* ctx, const LogitsArgs& a, int grid) {
                                   static_cast<int>(smem)));
     configured = true;
   }
-  k_logits<RB, CB, PARITY, VEC, NS><<<grid, kLT, smem, ctx->stream>>>(a);
+  LSB_CUDA(launch_pdl(ctx, k_logits<RB, CB, PARITY, VEC, NS>, dim3(grid), dim3(kLT), smem, a));
   LSB_LAUNCHED(ctx, "k_logits");
   return LSB_OK;
 }

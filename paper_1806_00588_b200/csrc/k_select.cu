@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(kSelT) k_softmax_topb(SoftmaxArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int row = blockIdx.x;
   const int s = row / a.Bsent, i = row % a.Bsent;
+  pdl_wait();
   const bool live = !(a.n_hyp && i >= a.n_hyp[s]) && !(a.finished && a.finished[row]);
   if (!live) {
     if (tid == 0) a.top_n[row] = 0;
@@ -262,7 +263,7 @@ lsb_status launch_softmax(lsb_ctx* ctx, const SoftmaxArgs& a) {
                                   static_cast<int>(smem)));
     configured = smem;
   }
-  k_softmax_topb<<<a.R_total, kSelT, smem, ctx->stream>>>(a);
+  LSB_CUDA(launch_pdl(ctx, k_softmax_topb, dim3(a.R_total), dim3(kSelT), smem, a));
   LSB_LAUNCHED(ctx, "k_softmax_topb");
   return LSB_OK;
 }
@@ -353,6 +354,7 @@ __global__ void __launch_bounds__(kExpT) k_expand(ExpandArgs a) {
   __shared__ int s_off[kRankMaxLists + 1];
   __shared__ uint32_t s_beams[64];
   __shared__ int s_count;
+  pdl_wait();
   const int s = blockIdx.x;
   const int R = a.Bsent;
   const int nfz = a.frozen_mode ? a.nfrozen : 0;
@@ -882,7 +884,7 @@ lsb_status launch_expand(lsb_ctx* ctx, const ExpandArgs& a) {
                                     static_cast<int>(rank_smem)));
       configured = rank_smem;
     }
-    k_expand<<<a.S, kExpT, rank_smem, ctx->stream>>>(a);  // kExpT threads per sentence
+    LSB_CUDA(launch_pdl(ctx, k_expand, dim3(a.S), dim3(kExpT), rank_smem, a));
     LSB_LAUNCHED(ctx, "k_expand");
     return LSB_OK;
   }

@@ -26,6 +26,7 @@ __global__ void __launch_bounds__(512) k_probe_count(ProbeArgs a) {
   const IndexView& ix = a.ix;
   const int row = blockIdx.x;
   const int s = row / a.B, i = row % a.B;
+  pdl_wait();
   if (a.n_hyp && i >= a.n_hyp[s]) return;
   if (a.finished && a.finished[row]) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
@@ -185,7 +186,7 @@ lsb_status launch_probe(lsb_ctx* ctx, const ProbeArgs& a) {
   dim3 grid(a.S * a.B, std::max(1u, nslices));
   // bit-sliced counters need little shared memory: 256-thread CTAs, 8 per SM,
   // so a 768-row step runs in one wave
-  k_probe_count<<<grid, a.levels >= 0 ? 256 : 512, smem, ctx->stream>>>(a);
+  LSB_CUDA(launch_pdl(ctx, k_probe_count, grid, dim3(a.levels >= 0 ? 256 : 512), smem, a));
   LSB_LAUNCHED(ctx, "k_probe_count");
   return LSB_OK;
 }
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
   __shared__ uint32_t wsum[33];
   __shared__ uint32_t s_thr, s_below, s_spec;
   const int s = blockIdx.x;
+  pdl_wait();
   uint32_t* ids = a.ids + static_cast<size_t>(s) * a.ncap;
   if (a.mode != 0) {
     // t == 0 (every word survives, src/candidate_selector.cpp:21-27) or
@@ -322,7 +324,7 @@ lsb_status launch_compact(lsb_ctx* ctx, const CompactArgs& a, int S) {
                                   static_cast<int>(smem)));
     configured = smem;
   }
-  k_compact<<<S, 1024, smem, ctx->stream>>>(a);
+  LSB_CUDA(launch_pdl(ctx, k_compact, dim3(S), dim3(1024), smem, a));
   LSB_LAUNCHED(ctx, "k_compact");
   return LSB_OK;
 }

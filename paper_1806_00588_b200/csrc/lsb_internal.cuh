@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "lshbeam_b200.h"
@@ -59,6 +60,7 @@ struct lsb_ctx {
   uint32_t* err_host = nullptr;  // pinned mirror
   uint64_t launches = 0;
   int cuckoo_parallel = 0;        // 0: reference slot placement
+  int pdl = 1;                    // programmatic dependent launch between step kernels
 };
 
 struct lsb_model {
@@ -106,6 +108,29 @@ struct lsb_index {
 
 // ------------------------------------------------------ device helpers
 namespace lsb {
+
+// Programmatic dependent launch: a step kernel launched with
+// launch_pdl() may start (launch, set up shared memory, compute addresses)
+// while its predecessor on the stream drains; pdl_wait() blocks until the
+// predecessor's results are visible and must precede every read of them.
+// Without the launch attribute it returns immediately.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(lsb_ctx* ctx, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = ctx->pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 __device__ __forceinline__ uint32_t slot_of(unsigned long long mul, uint32_t lg,
                                             uint32_t key) {

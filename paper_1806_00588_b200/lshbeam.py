@@ -329,8 +329,9 @@ class Batch:
     def keep_probs(self, on: bool = True):
         N.check(self.lib.lsb_batch_keep_probs(self.h, int(on)))
 
-    def profile(self, on: bool = True):
-        N.check(self.lib.lsb_batch_profile(self.h, int(on)))
+    def profile(self, on: bool = True, every: int = 1):
+        """Per-stage CUDA events; ``every`` > 1 samples every n-th step."""
+        N.check(self.lib.lsb_batch_profile(self.h, (every if every > 1 else 1) if on else 0))
 
     def stage_ms(self) -> np.ndarray:
         out = np.zeros(5, np.float32)
