@@ -234,6 +234,15 @@ typedef struct lsb_state_host {
 lsb_status lsb_step_host(lsb_batch* b, const lsb_state_host* in, lsb_choice* choices_host,
                          int32_t* n_choices_host, float* hidden_out_host);
 
+/* Pipelined form of lsb_step_host for a stream of steps: enqueues the
+ * uploads on an internal copy stream (two staging slots, so step k+1's
+ * upload overlaps step k's kernels), the step, and the read-back of the
+ * choices into the caller's (pinned) buffers; does not synchronise. The
+ * host buffers must stay valid until lsb_batch_wait returns. */
+lsb_status lsb_step_host_async(lsb_batch* b, const lsb_state_host* in, lsb_choice* choices_host,
+                               int32_t* n_choices_host);
+lsb_status lsb_batch_wait(lsb_batch* b);   /* drain + surface device errors */
+
 /* Per-sentence views of the last step (device -> host copies, synchronous):
  * candidate ids (|V_LSH| of them, ascending), provenance
  * {from_threshold, from_top, from_specials}, query band codes

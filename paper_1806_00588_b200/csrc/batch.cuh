@@ -46,6 +46,20 @@ struct lsb_batch {
   lsb_choice* h_choices = nullptr;
   int32_t* h_nchoices = nullptr;
   float* h_hidden_out = nullptr;
+  // pipelined host-buffer steps (lsb_step_host_async): two staging slots, a
+  // copy stream for the uploads, events ordering uploads and kernels
+  struct AsyncSlot {
+    float* hidden = nullptr;
+    double* scores = nullptr;
+    uint8_t* finished = nullptr;
+    int32_t* n_hyp = nullptr;
+    lsb_choice* choices = nullptr;
+    int32_t* n_choices = nullptr;
+    cudaEvent_t uploaded = nullptr, consumed = nullptr;
+    bool used = false;
+  } slot[2];
+  cudaStream_t copy_stream = nullptr;
+  int next_slot = 0;
   // last step (for the per-sentence views)
   lsb_state_dev last{};
   bool has_last = false;

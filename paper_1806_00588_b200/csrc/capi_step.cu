@@ -31,6 +31,14 @@ lsb_status free_batch(lsb_batch* b) {
                   b->h_hidden_out, b->sh_top, b->sh_topn, b->tc_A, b->tc_H, b->arrive};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (auto& sl : b->slot) {
+    void* sp[] = {sl.hidden, sl.scores, sl.finished, sl.n_hyp, sl.choices, sl.n_choices};
+    for (void* p : sp)
+      if (p) cudaFree(p);
+    if (sl.uploaded) cudaEventDestroy(sl.uploaded);
+    if (sl.consumed) cudaEventDestroy(sl.consumed);
+  }
+  if (b->copy_stream) cudaStreamDestroy(b->copy_stream);
   for (auto& e : b->ring)
     if (e) cudaEventDestroy(e);
   delete b;
@@ -374,6 +382,68 @@ lsb_status lsb_step_host(lsb_batch* b, const lsb_state_host* in, lsb_choice* cho
   LSB_CUDA(cudaMemcpyAsync(n_choices_host, b->h_nchoices, b->S * 4, cudaMemcpyDeviceToHost, st));
   if (hidden_out_host)
     LSB_CUDA(cudaMemcpyAsync(hidden_out_host, b->h_hidden_out, HD * 4, cudaMemcpyDeviceToHost, st));
+  return lsb_ctx_sync(b->ctx);
+}
+
+// Pipelined variant of lsb_step_host: uploads go to a copy stream into one
+// of two staging slots while the previous step's kernels run; the step waits
+// for its upload, and its choices are read back (D2H) on the step stream.
+// Nothing synchronises the host; lsb_batch_wait drains the pipeline.
+lsb_status lsb_step_host_async(lsb_batch* b, const lsb_state_host* in, lsb_choice* choices_host,
+                               int32_t* n_choices_host) {
+  if (!b || !in || !in->hidden || !in->scores || !choices_host || !n_choices_host)
+    return set_error("lsb_step_host_async: null argument"), LSB_EINVAL;
+  const size_t SB = static_cast<size_t>(b->S) * b->B;
+  const size_t HD = SB * b->d;
+  cudaStream_t st = b->ctx->stream;
+  if (!b->copy_stream) {
+    LSB_CUDA(cudaStreamCreateWithFlags(&b->copy_stream, cudaStreamNonBlocking));
+    for (auto& sl : b->slot) {
+      LSB_CUDA(dalloc(&sl.hidden, HD));
+      LSB_CUDA(dalloc(&sl.scores, SB));
+      LSB_CUDA(dalloc(&sl.finished, SB));
+      LSB_CUDA(dalloc(&sl.n_hyp, b->S));
+      LSB_CUDA(dalloc(&sl.choices, SB));
+      LSB_CUDA(dalloc(&sl.n_choices, b->S));
+      LSB_CUDA(cudaEventCreateWithFlags(&sl.uploaded, cudaEventDisableTiming));
+      LSB_CUDA(cudaEventCreateWithFlags(&sl.consumed, cudaEventDisableTiming));
+    }
+  }
+  auto& sl = b->slot[b->next_slot];
+  b->next_slot ^= 1;
+  cudaStream_t cs = b->copy_stream;
+  // the step that used this slot two calls ago must be done reading it
+  if (sl.used) LSB_CUDA(cudaStreamWaitEvent(cs, sl.consumed, 0));
+  LSB_CUDA(cudaMemcpyAsync(sl.hidden, in->hidden, HD * 4, cudaMemcpyHostToDevice, cs));
+  LSB_CUDA(cudaMemcpyAsync(sl.scores, in->scores, SB * 8, cudaMemcpyHostToDevice, cs));
+  lsb_state_dev d{};
+  d.hidden = sl.hidden;
+  d.scores = sl.scores;
+  if (in->finished) {
+    LSB_CUDA(cudaMemcpyAsync(sl.finished, in->finished, SB, cudaMemcpyHostToDevice, cs));
+    d.finished = sl.finished;
+  }
+  if (in->n_hyp) {
+    LSB_CUDA(cudaMemcpyAsync(sl.n_hyp, in->n_hyp, b->S * 4, cudaMemcpyHostToDevice, cs));
+    d.n_hyp = sl.n_hyp;
+  }
+  LSB_CUDA(cudaEventRecord(sl.uploaded, cs));
+  LSB_CUDA(cudaStreamWaitEvent(st, sl.uploaded, 0));
+  lsb_out_dev o{};
+  o.choices = sl.choices;
+  o.n_choices = sl.n_choices;
+  lsb_status rc = lsb_step(b, &d, &o);
+  if (rc) return rc;
+  LSB_CUDA(cudaEventRecord(sl.consumed, st));
+  sl.used = true;
+  LSB_CUDA(cudaMemcpyAsync(choices_host, sl.choices, SB * sizeof(lsb_choice),
+                           cudaMemcpyDeviceToHost, st));
+  LSB_CUDA(cudaMemcpyAsync(n_choices_host, sl.n_choices, b->S * 4, cudaMemcpyDeviceToHost, st));
+  return LSB_OK;
+}
+
+lsb_status lsb_batch_wait(lsb_batch* b) {
+  if (!b) return set_error("lsb_batch_wait: null"), LSB_EINVAL;
   return lsb_ctx_sync(b->ctx);
 }
 

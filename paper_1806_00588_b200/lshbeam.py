@@ -352,6 +352,15 @@ class Batch:
         N.check(self.lib.lsb_step_host(self.h, C.byref(st), choices, n_choices,
                                        hidden_out or None), "lsb_step_host")
 
+    def step_host_async(self, hidden, scores, finished, n_hyp, choices, n_choices):
+        """lsb_step_host_async with raw (pinned) host pointers; call wait()."""
+        st = N.lsb_state_host(hidden, scores, finished or None, n_hyp or None)
+        N.check(self.lib.lsb_step_host_async(self.h, C.byref(st), choices, n_choices),
+                "lsb_step_host_async")
+
+    def wait(self):
+        N.check(self.lib.lsb_batch_wait(self.h), "lsb_batch_wait")
+
     def step(self, hidden, scores, finished=None, n_hyp=None, choices=None, n_choices=None,
              hidden_out=None):
         """Device step. Arguments are torch CUDA tensors (or raw pointers):

@@ -152,3 +152,39 @@ def test_batch_config_validation(ctx, oracle):
         Batch(ctx, m, idx, S=1, B=4, specials=[300])
     with pytest.raises(ValueError):
         Batch(ctx, m, None, S=1, B=4)  # lsh mode requires an index
+
+
+def test_step_host_async_matches_sync(ctx, oracle):
+    """The pipelined host-buffer API (two staging slots, copy stream) gives the
+    same choices as the synchronous one over a sequence of distinct steps."""
+    import ctypes as C
+
+    import torch
+    from paper_1806_00588_b200 import _native as N
+    V, d, K, u, W, S, B, T, t = 3000, 64, 8, 3, 16, 4, 12, 100, 2
+    E, bias, perms, bt, ps, isd = make_world(oracle, V, d, K, u, W, seed=21, bias_strength=4.0)
+    from paper_1806_00588_b200 import Batch, Index, Model
+    m = Model(ctx, E, bias)
+    idx = Index(ctx, m, K=K, u=u, W=W, perm_seed=ps, index_seed=isd)
+    b = Batch(ctx, m, idx, S=S, B=B, T=T, t=t, specials=[V - 1])
+    steps = 5
+    states = [make_state(oracle, S, B, d, seed=100 + k, frozen_every=3 if k % 2 else 0)
+              for k in range(steps)]
+    want = [b.step_host(*st)[0] for st in states]
+    pinned = []
+    outs = []
+    for st in states:
+        hidden, scores, finished, n_hyp = (torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+                                           for x in st)
+        ch = (N.lsb_choice * (S * B))()
+        nc = np.zeros(S, np.int32)
+        pinned.append((hidden, scores, finished, n_hyp))
+        outs.append((ch, nc))
+        b.step_host_async(hidden.data_ptr(), scores.data_ptr(), finished.data_ptr(),
+                          n_hyp.data_ptr(), ch, nc.ctypes.data_as(C.c_void_p))
+    b.wait()
+    for k in range(steps):
+        ch, nc = outs[k]
+        got = [[(ch[s * B + j].score, ch[s * B + j].beam, ch[s * B + j].word)
+                for j in range(int(nc[s]))] for s in range(S)]
+        assert got == want[k]
