@@ -30,8 +30,9 @@
 namespace lsb {
 
 constexpr int kLT = 128;        // threads per CTA
-constexpr int kKC = 32;         // floats of d per pipeline stage
-constexpr int kKS = kKC + 4;    // shared-memory row pitch in floats
+// d is staged in chunks of KC floats (32, or 16 for 2-column tiles); the
+// shared-memory row pitch KC + 4 floats is 4 mod 32 words for KC = 32 and
+// 20 for KC = 16 -- both conflict-free for 16-byte loads by 8-thread phases.
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
@@ -49,23 +50,23 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-template <int RB, int CB, int NS>
+template <int RB, int CB, int NS, int KC>
 constexpr size_t logits_smem_bytes() {
-  return static_cast<size_t>(NS) * (kLT * CB + RB) * kKS * 4 + kLT * CB * 4;
+  return static_cast<size_t>(NS) * (kLT * CB + RB) * (KC + 4) * 4 + kLT * CB * 4;
 }
 
 // One 4-wide step of d for RB rows x CB columns: float4 of H (smem
 // broadcast) times float4 of each column's E row.
-template <int RB, int CB, bool PARITY>
+template <int RB, int CB, bool PARITY, int KS>
 __device__ __forceinline__ void mac4(float (&acc)[RB][CB][PARITY ? 4 : 1], const float* Es,
                                      const float* Hs, int tid, int k4) {
   float4 e[CB];
 #pragma unroll
   for (int cb = 0; cb < CB; ++cb)
-    e[cb] = *reinterpret_cast<const float4*>(Es + (tid + cb * kLT) * kKS + k4 * 4);
+    e[cb] = *reinterpret_cast<const float4*>(Es + (tid + cb * kLT) * KS + k4 * 4);
 #pragma unroll
   for (int rb = 0; rb < RB; ++rb) {
-    const float4 h = *reinterpret_cast<const float4*>(Hs + rb * kKS + k4 * 4);
+    const float4 h = *reinterpret_cast<const float4*>(Hs + rb * KS + k4 * 4);
 #pragma unroll
     for (int cb = 0; cb < CB; ++cb) {
       if constexpr (PARITY) {
@@ -100,17 +101,17 @@ __device__ __forceinline__ unsigned long long f2fma(unsigned long long a, unsign
   return d;
 }
 
-template <int RB, int CB>
+template <int RB, int CB, int KS>
 __device__ __forceinline__ void mac4_x2(unsigned long long (&acc)[RB][CB][2], const float* Es,
                                         const float* Hs, int tid, int k4,
                                         unsigned long long negz, unsigned long long one) {
   ulonglong2 e[CB];
 #pragma unroll
   for (int cb = 0; cb < CB; ++cb)
-    e[cb] = *reinterpret_cast<const ulonglong2*>(Es + (tid + cb * kLT) * kKS + k4 * 4);
+    e[cb] = *reinterpret_cast<const ulonglong2*>(Es + (tid + cb * kLT) * KS + k4 * 4);
 #pragma unroll
   for (int rb = 0; rb < RB; ++rb) {
-    const ulonglong2 h = *reinterpret_cast<const ulonglong2*>(Hs + rb * kKS + k4 * 4);
+    const ulonglong2 h = *reinterpret_cast<const ulonglong2*>(Hs + rb * KS + k4 * 4);
 #pragma unroll
     for (int cb = 0; cb < CB; ++cb) {
       acc[rb][cb][0] = f2fma(acc[rb][cb][0], one, f2fma(h.x, e[cb].x, negz));
@@ -119,8 +120,12 @@ __device__ __forceinline__ void mac4_x2(unsigned long long (&acc)[RB][CB][2], co
   }
 }
 
-template <int RB, int CB, bool PARITY, bool VEC, int kStages>
+template <int RB, int CB, bool PARITY, bool VEC, int kStages, int KC>
 __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs a) {
+  constexpr int kKC = KC;
+  constexpr int kKS = KC + 4;
+  constexpr int kParts = KC / 4;           // 16-byte pieces per row chunk
+  constexpr int kRowStep = kLT / kParts;   // rows covered by one pass of the CTA
   extern __shared__ __align__(16) float sm[];
   constexpr int CT = kLT * CB;
   constexpr int STAGE = (CT + RB) * kKS;
@@ -167,7 +172,7 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
     // per-tile source offsets (elements) of this thread's 16-byte pieces:
     // piece i covers column (tid >> 3) + 16 i, floats [4 (tid & 7), +4) of
     // every chunk; invalid columns / rows carry bit 31 and are zero-filled
-    const int part = tid & 7;
+    const int part = tid % kParts;
     // sid[] now holds each column's element offset sid*d (bit 31 = invalid),
     // re-read per chunk instead of pinning 8 registers per thread
     if constexpr (VEC) {
@@ -176,8 +181,8 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
         sid[c] = c < ncols ? sid[c] * static_cast<uint32_t>(d) : 0x80000000u;
       __syncthreads();
     }
-    const int hrow = tid >> 3;
-    const uint32_t hoff = (tid < RB * 8 && row0 + hrow < rowlim)
+    const int hrow = tid / kParts;
+    const uint32_t hoff = (tid < RB * kParts && row0 + hrow < rowlim)
                               ? static_cast<uint32_t>(row0 + hrow) * d + part * 4
                               : 0x80000000u;
 
@@ -188,25 +193,25 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
       if constexpr (VEC) {
         const bool kin = c0 + part * 4 < d;
 #pragma unroll
-        for (int i = 0; i < 8 * CB; ++i) {
-          const uint32_t off = sid[(tid >> 3) + 16 * i];
+        for (int i = 0; i < CT / kRowStep; ++i) {
+          const int col = tid / kParts + kRowStep * i;
+          const uint32_t off = sid[col];
           const bool ok = kin && !(off & 0x80000000u);
-          cp_async16(Es + ((tid >> 3) + 16 * i) * kKS + part * 4,
-                     a.E + (ok ? off + part * 4 + c0 : 0), ok ? 16 : 0);
+          cp_async16(Es + col * kKS + part * 4, a.E + (ok ? off + part * 4 + c0 : 0), ok ? 16 : 0);
         }
-        if (tid < RB * 8) {
+        if (tid < RB * kParts) {
           const bool ok = kin && !(hoff & 0x80000000u);
           cp_async16(Hs + hrow * kKS + part * 4, a.H + (ok ? hoff + c0 : 0), ok ? 16 : 0);
         }
       } else {
         for (int q = tid; q < CT * kKC; q += kLT) {
-          const int col = q >> 5, kk = q & 31;
+          const int col = q / kKC, kk = q % kKC;
           const bool ok = col < ncols && c0 + kk < d;
           const float* src = ok ? a.E + static_cast<size_t>(sid[col]) * d + c0 + kk : a.E;
           cp_async4(Es + col * kKS + kk, src, ok ? 4 : 0);
         }
         for (int q = tid; q < RB * kKC; q += kLT) {
-          const int rb = q >> 5, kk = q & 31;
+          const int rb = q / kKC, kk = q % kKC;
           const bool ok = row0 + rb < rowlim && c0 + kk < d;
           const float* src = ok ? a.H + static_cast<size_t>(row0 + rb) * d + c0 + kk : a.H;
           cp_async4(Hs + rb * kKS + kk, src, ok ? 4 : 0);
@@ -256,19 +261,19 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
             if (kv == kKC / 4) {
 #pragma unroll
             for (int k4 = 0; k4 < kKC / 4; ++k4)
-                mac4_x2<RB, CB>(acc2, Es, Hs, tid, k4, a.x2_negzero, a.x2_one);
+                mac4_x2<RB, CB, kKS>(acc2, Es, Hs, tid, k4, a.x2_negzero, a.x2_one);
             } else {
               for (int k4 = 0; k4 < kv; ++k4)
-                mac4_x2<RB, CB>(acc2, Es, Hs, tid, k4, a.x2_negzero, a.x2_one);
+                mac4_x2<RB, CB, kKS>(acc2, Es, Hs, tid, k4, a.x2_negzero, a.x2_one);
             }
           }
         }
         if (!done) {
           if (kv == kKC / 4) {
 #pragma unroll
-            for (int k4 = 0; k4 < kKC / 4; ++k4) mac4<RB, CB, PARITY>(acc, Es, Hs, tid, k4);
+            for (int k4 = 0; k4 < kKC / 4; ++k4) mac4<RB, CB, PARITY, kKS>(acc, Es, Hs, tid, k4);
           } else {
-            for (int k4 = 0; k4 < kv; ++k4) mac4<RB, CB, PARITY>(acc, Es, Hs, tid, k4);
+            for (int k4 = 0; k4 < kv; ++k4) mac4<RB, CB, PARITY, kKS>(acc, Es, Hs, tid, k4);
           }
         }
       }
@@ -349,22 +354,22 @@ int choose_rb(int B) {
   return best;
 }
 
-template <int RB, int CB, bool PARITY, bool VEC, int NS>
+template <int RB, int CB, bool PARITY, bool VEC, int NS, int KC = 32>
 static lsb_status launch_variant(lsb_ctx* ctx, const LogitsArgs& a, int grid) {
-  constexpr size_t smem = logits_smem_bytes<RB, CB, NS>();
+  constexpr size_t smem = logits_smem_bytes<RB, CB, NS, KC>();
   static bool configured = false;
   if (!configured) {
-    LSB_CUDA(cudaFuncSetAttribute(k_logits<RB, CB, PARITY, VEC, NS>,
+    LSB_CUDA(cudaFuncSetAttribute(k_logits<RB, CB, PARITY, VEC, NS, KC>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     configured = true;
   }
-  LSB_CUDA(launch_pdl(ctx, k_logits<RB, CB, PARITY, VEC, NS>, dim3(grid), dim3(kLT), smem, a));
+  LSB_CUDA(launch_pdl(ctx, k_logits<RB, CB, PARITY, VEC, NS, KC>, dim3(grid), dim3(kLT), smem, a));
   LSB_LAUNCHED(ctx, "k_logits");
   return LSB_OK;
 }
 
-template <int RB, int CB, bool PARITY>
+template <int RB, int CB, bool PARITY, int KC = 32>
 static lsb_status launch_logits_rb(lsb_ctx* ctx, LogitsArgs a, int target) {
   constexpr int CT = kLT * CB;
   const int rgroups = (a.R_total + RB - 1) / RB;
@@ -385,10 +390,10 @@ static lsb_status launch_logits_rb(lsb_ctx* ctx, LogitsArgs a, int target) {
   // Survivor-only launches (the shared block went to the tensor cores) have
   // no other CTAs to hide their L2 latency behind: 3-stage ring instead of 2.
   if (a.skip_shared)
-    return vec ? launch_variant<RB, CB, PARITY, true, 3>(ctx, a, grid)
-               : launch_variant<RB, CB, PARITY, false, 3>(ctx, a, grid);
-  return vec ? launch_variant<RB, CB, PARITY, true, 2>(ctx, a, grid)
-             : launch_variant<RB, CB, PARITY, false, 2>(ctx, a, grid);
+    return vec ? launch_variant<RB, CB, PARITY, true, 3, KC>(ctx, a, grid)
+               : launch_variant<RB, CB, PARITY, false, 3, KC>(ctx, a, grid);
+  return vec ? launch_variant<RB, CB, PARITY, true, 2, KC>(ctx, a, grid)
+             : launch_variant<RB, CB, PARITY, false, 2, KC>(ctx, a, grid);
 }
 
 // One column per thread, RB rows: 8 FP instructions (PARITY) or 4 FFMA
@@ -422,6 +427,9 @@ lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_c
   case R:                                                                \
     return fast ? launch_logits_rb<R, 1, false>(ctx, a, target_ctas)     \
                 : launch_logits_rb<R, 1, true>(ctx, a, target_ctas);
+  // (A 6-row x 2-column tile with 16-float chunks halves the H loads per
+  // FFMA2 but measured 151 us vs 121 us at cfg 2: more E-tile refills and
+  // spills; the 12 x 1 tile stays.)
   switch (choose_rb(a.Bsent)) {
     LSB_RB(16)
     LSB_RB(12)
