@@ -71,6 +71,7 @@ def build(verbose: bool = False) -> str:
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
     build_cpp()
+    build_cli()
     if verbose:
         print(LIB)
         print(CPPLIB)
@@ -92,6 +93,27 @@ def build_cpp() -> str:
     if r.returncode != 0:
         raise RuntimeError(f"C++ drop-in build failed:\n{r.stderr}")
     return CPPLIB
+
+
+CLI_SRC = os.path.join(PKG, "cli", "lshbeam_main.cpp")
+CLI_BIN = os.path.join(PKG, "lshbeam")
+JSON_INC = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
+
+
+def build_cli() -> str | None:
+    """The `lshbeam` CLI (build/decode/grid) over liblshbeam.so. Needs
+    nlohmann/json (vendored by cudnn-frontend in this image); skipped if absent."""
+    if not os.path.exists(os.path.join(JSON_INC, "json.hpp")):
+        return None
+    deps = [CLI_SRC, CPPLIB, __file__]
+    if _newer(CLI_BIN, deps):
+        return CLI_BIN
+    cmd = [CXX, *CXXFLAGS, "-I" + JSON_INC, "-o", CLI_BIN, CLI_SRC, "-L" + PKG, "-llshbeam",
+           "-llshbeam_b200", "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"CLI build failed:\n{r.stderr}")
+    return CLI_BIN
 
 
 if __name__ == "__main__":

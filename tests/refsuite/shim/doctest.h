@@ -2,7 +2,8 @@
 // The reference's unit suites (/root/reference/proj/tests/test_*.cpp) include
 // "doctest.h", which the reference does not ship (proj/vendor/ is absent).
 // This shim implements the subset they use -- TEST_CASE, CHECK, REQUIRE,
-// CHECK_THROWS_AS, CHECK_NOTHROW, doctest::Approx(...).epsilon().scale() --
+// REQUIRE_MESSAGE, CHECK_THROWS_AS, CHECK_NOTHROW, doctest::Approx(...).epsilon()
+// .scale() --
 // so those suites compile unchanged against the GPU build's drop-in headers.
 #pragma once
 
@@ -118,6 +119,10 @@ inline int run_all() {
 #define REQUIRE(...) \
   ::doctest::shim::check(static_cast<bool>(__VA_ARGS__), #__VA_ARGS__, __FILE__, __LINE__, true)
 #define CHECK_FALSE(...) CHECK(!(__VA_ARGS__))
+#define REQUIRE_MESSAGE(cond, msg) \
+  ::doctest::shim::check(static_cast<bool>(cond), #cond " (" msg ")", __FILE__, __LINE__, true)
+#define CHECK_MESSAGE(cond, msg) \
+  ::doctest::shim::check(static_cast<bool>(cond), #cond " (" msg ")", __FILE__, __LINE__, false)
 #define FAIL(msg) ::doctest::shim::check(false, "FAIL", __FILE__, __LINE__, true)
 
 // CHECK_THROWS_AS(expression..., ExceptionType): the expression may contain

@@ -32,11 +32,30 @@ def test_reference_suite_on_gpu(suite):
     assert "| 0 failed" in r.stdout, tail
 
 
+CLI = os.path.join(os.path.dirname(HERE), "paper_1806_00588_b200", "lshbeam")
+
+
+def test_reference_cli_suite():
+    """test_cli.cpp (11 cases: exit codes, deterministic index bytes,
+    full == lsh(t=0) == lsh(T=V) through JSON reports, grid CSV layout,
+    determinism across worker counts) against our `lshbeam` CLI."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    exe = os.path.join(BUILD, "test_cli")
+    if not (os.path.exists(exe) and os.path.exists(CLI)):
+        pytest.skip("test_cli or the lshbeam CLI not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900, cwd=BUILD,
+                       env={**os.environ, "LSHBEAM_CLI": CLI})
+    tail = "\n".join((r.stdout + r.stderr).splitlines()[-40:])
+    assert r.returncode == 0 and "| 0 failed" in r.stdout, tail
+
+
 def test_reference_acceptance_criteria_1_to_8():
     """acceptance.cpp (criteria 1-8: oracle equivalence over 100 seeds, cuckoo at
     load 0.5, hit matrix vs brute force, rank correlation, |V_LSH| / recall grid,
-    softmax-path speedup at B=12 and B=48, top-T effect) against the GPU build.
-    Criterion 9 drives the reference CLI (out of scope, not built)."""
+    softmax-path speedup at B=12 and B=48, top-T effect, and criterion 9, CLI
+    determinism, through our `lshbeam` CLI) against the GPU build."""
     import re
 
     import torch
@@ -45,8 +64,8 @@ def test_reference_acceptance_criteria_1_to_8():
     exe = os.path.join(BUILD, "acceptance")
     if not os.path.exists(exe):
         pytest.skip("acceptance not built")
-    r = subprocess.run([exe, "/nonexistent/lshbeam_cli"], capture_output=True, text=True,
-                       timeout=1500, cwd=BUILD)
+    cli = CLI if os.path.exists(CLI) else "/nonexistent/lshbeam_cli"
+    r = subprocess.run([exe, cli], capture_output=True, text=True, timeout=1500, cwd=BUILD)
     status = dict(re.findall(r"criterion (\d+): (PASS|FAIL)", r.stdout))
-    for c in map(str, range(1, 9)):
+    for c in map(str, range(1, 10 if os.path.exists(CLI) else 9)):
         assert status.get(c) == "PASS", r.stdout[-3000:]
