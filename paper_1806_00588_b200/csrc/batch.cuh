@@ -55,10 +55,11 @@ struct lsb_batch {
     int32_t* n_hyp = nullptr;
     lsb_choice* choices = nullptr;
     int32_t* n_choices = nullptr;
-    cudaEvent_t uploaded = nullptr, consumed = nullptr;
+    cudaEvent_t uploaded = nullptr, computed = nullptr, consumed = nullptr;
     bool used = false;
   } slot[2];
-  cudaStream_t copy_stream = nullptr;
+  cudaStream_t copy_stream = nullptr;   // uploads
+  cudaStream_t down_stream = nullptr;   // read-backs
   int next_slot = 0;
   // last step (for the per-sentence views)
   lsb_state_dev last{};

@@ -37,8 +37,10 @@ lsb_status free_batch(lsb_batch* b) {
       if (p) cudaFree(p);
     if (sl.uploaded) cudaEventDestroy(sl.uploaded);
     if (sl.consumed) cudaEventDestroy(sl.consumed);
+    if (sl.computed) cudaEventDestroy(sl.computed);
   }
   if (b->copy_stream) cudaStreamDestroy(b->copy_stream);
+  if (b->down_stream) cudaStreamDestroy(b->down_stream);
   for (auto& e : b->ring)
     if (e) cudaEventDestroy(e);
   delete b;
@@ -385,9 +387,10 @@ lsb_status lsb_step_host(lsb_batch* b, const lsb_state_host* in, lsb_choice* cho
   return lsb_ctx_sync(b->ctx);
 }
 
-// Pipelined variant of lsb_step_host: uploads go to a copy stream into one
-// of two staging slots while the previous step's kernels run; the step waits
-// for its upload, and its choices are read back (D2H) on the step stream.
+// Pipelined variant of lsb_step_host: uploads go to an upload stream into
+// one of two staging slots while the previous step's kernels run; the step
+// waits for its upload; its choices are read back on a third stream, so the
+// step stream runs kernels only.
 // Nothing synchronises the host; lsb_batch_wait drains the pipeline.
 lsb_status lsb_step_host_async(lsb_batch* b, const lsb_state_host* in, lsb_choice* choices_host,
                                int32_t* n_choices_host) {
@@ -398,6 +401,7 @@ lsb_status lsb_step_host_async(lsb_batch* b, const lsb_state_host* in, lsb_choic
   cudaStream_t st = b->ctx->stream;
   if (!b->copy_stream) {
     LSB_CUDA(cudaStreamCreateWithFlags(&b->copy_stream, cudaStreamNonBlocking));
+    LSB_CUDA(cudaStreamCreateWithFlags(&b->down_stream, cudaStreamNonBlocking));
     for (auto& sl : b->slot) {
       LSB_CUDA(dalloc(&sl.hidden, HD));
       LSB_CUDA(dalloc(&sl.scores, SB));
@@ -407,6 +411,7 @@ lsb_status lsb_step_host_async(lsb_batch* b, const lsb_state_host* in, lsb_choic
       LSB_CUDA(dalloc(&sl.n_choices, b->S));
       LSB_CUDA(cudaEventCreateWithFlags(&sl.uploaded, cudaEventDisableTiming));
       LSB_CUDA(cudaEventCreateWithFlags(&sl.consumed, cudaEventDisableTiming));
+      LSB_CUDA(cudaEventCreateWithFlags(&sl.computed, cudaEventDisableTiming));
     }
   }
   auto& sl = b->slot[b->next_slot];
@@ -434,16 +439,24 @@ lsb_status lsb_step_host_async(lsb_batch* b, const lsb_state_host* in, lsb_choic
   o.n_choices = sl.n_choices;
   lsb_status rc = lsb_step(b, &d, &o);
   if (rc) return rc;
-  LSB_CUDA(cudaEventRecord(sl.consumed, st));
-  sl.used = true;
+  // read-back on the copy stream, so the step stream goes straight on to the
+  // next step; `consumed` then covers both the kernels' reads of the staged
+  // inputs and the read-back of the staged outputs
+  cudaStream_t ds = b->down_stream;
+  LSB_CUDA(cudaEventRecord(sl.computed, st));
+  LSB_CUDA(cudaStreamWaitEvent(ds, sl.computed, 0));
   LSB_CUDA(cudaMemcpyAsync(choices_host, sl.choices, SB * sizeof(lsb_choice),
-                           cudaMemcpyDeviceToHost, st));
-  LSB_CUDA(cudaMemcpyAsync(n_choices_host, sl.n_choices, b->S * 4, cudaMemcpyDeviceToHost, st));
+                           cudaMemcpyDeviceToHost, ds));
+  LSB_CUDA(cudaMemcpyAsync(n_choices_host, sl.n_choices, b->S * 4, cudaMemcpyDeviceToHost, ds));
+  LSB_CUDA(cudaEventRecord(sl.consumed, ds));
+  sl.used = true;
   return LSB_OK;
 }
 
 lsb_status lsb_batch_wait(lsb_batch* b) {
   if (!b) return set_error("lsb_batch_wait: null"), LSB_EINVAL;
+  if (b->copy_stream) LSB_CUDA(cudaStreamSynchronize(b->copy_stream));
+  if (b->down_stream) LSB_CUDA(cudaStreamSynchronize(b->down_stream));
   return lsb_ctx_sync(b->ctx);
 }
 
