@@ -53,6 +53,7 @@ __device__ __forceinline__ T block_reduce(T v, T* red, Op op) {
 // arg-max by (p desc, column asc) in which only the owner of the winning
 // column rescans its registers. Same arithmetic as the general path.
 constexpr int kSelReg = 16;
+constexpr int kSelCand = 128;  // threshold survivors ranked directly
 
 __device__ __forceinline__ void row_registers(const SoftmaxArgs& a, int row, float* L, uint32_t n,
                                               float* red_f, double* red_d) {
@@ -97,6 +98,65 @@ __device__ __forceinline__ void row_registers(const SoftmaxArgs& a, int row, flo
     } else {
       v[k] = -1.0f;
     }
+  }
+  // Threshold filter: per warp, the B-th largest of the 32 lane maxima (a
+  // shuffle bitonic sort) is a lower bound for the row's B-th largest p, so
+  // is the maximum of those bounds over the warps; only entries >= it can be
+  // in the top-B. Usually a few dozen survive: rank them exactly in one warp.
+  {
+    __shared__ float s_tau[kSelT / 32];
+    __shared__ int s_nc;
+    __shared__ float c_p[kSelCand];
+    __shared__ uint32_t c_c[kSelCand];
+    float tm = -1.0f;
+#pragma unroll
+    for (int k = 0; k < kSelReg; ++k) tm = fmaxf(tm, v[k]);
+    float x = tm;  // bitonic sort of the warp's 32 lane maxima, descending
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1)
+#pragma unroll
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        const float y = __shfl_xor_sync(0xffffffffu, x, stride);
+        const bool up = ((lane & size) == 0) == ((lane & stride) == 0);
+        x = up ? fmaxf(x, y) : fminf(x, y);
+      }
+    const int bsel = min(a.topB, 32);
+    const float tau_w = __shfl_sync(0xffffffffu, x, bsel - 1);
+    if (lane == 0) s_tau[warp] = a.topB <= 32 ? tau_w : -1.0f;
+    if (tid == 0) s_nc = 0;
+    __syncthreads();
+    float tau = s_tau[0];
+#pragma unroll
+    for (int w = 1; w < kSelT / 32; ++w) tau = fmaxf(tau, s_tau[w]);
+    if (tau >= 0.0f) {
+#pragma unroll
+      for (int k = 0; k < kSelReg; ++k)
+        if (v[k] >= tau) {
+          const int at = atomicAdd(&s_nc, 1);
+          if (at < kSelCand) {
+            c_p[at] = v[k];
+            c_c[at] = tid + kSelT * k;
+          }
+        }
+    }
+    __syncthreads();
+    const int nc = s_nc;
+    const int keep = static_cast<int>(min(static_cast<uint32_t>(a.topB), n));
+    if (tau >= 0.0f && nc <= kSelCand && nc >= keep) {
+      if (warp == 0) {
+        TopEntry* out = a.top + static_cast<size_t>(row) * a.topB;
+        for (int q = lane; q < nc; q += 32) {
+          const float p = c_p[q];
+          const uint32_t c = c_c[q];
+          int rank = 0;
+          for (int j = 0; j < nc; ++j) rank += top_better(c_p[j], c_c[j], p, c);
+          if (rank < keep) out[rank] = TopEntry{p, c};
+        }
+        if (lane == 0) a.top_n[row] = keep;
+      }
+      return;
+    }
+    // (many ties at the threshold: fall through to the round-based merge)
   }
   float bp = -1.0f;
   int bk = 0;
