@@ -59,14 +59,14 @@ constexpr size_t logits_smem_bytes() {
 // broadcast) times float4 of each column's E row.
 template <int RB, int CB, bool PARITY, int KS>
 __device__ __forceinline__ void mac4(float (&acc)[RB][CB][PARITY ? 4 : 1], const float* Es,
-                                     const float* Hs, int tid, int k4) {
+                                     const float* Hs, int rbase, int cbase, int cstride, int k4) {
   float4 e[CB];
 #pragma unroll
   for (int cb = 0; cb < CB; ++cb)
-    e[cb] = *reinterpret_cast<const float4*>(Es + (tid + cb * kLT) * KS + k4 * 4);
+    e[cb] = *reinterpret_cast<const float4*>(Es + (cbase + cb * cstride) * KS + k4 * 4);
 #pragma unroll
   for (int rb = 0; rb < RB; ++rb) {
-    const float4 h = *reinterpret_cast<const float4*>(Hs + rb * KS + k4 * 4);
+    const float4 h = *reinterpret_cast<const float4*>(Hs + (rbase + rb) * KS + k4 * 4);
 #pragma unroll
     for (int cb = 0; cb < CB; ++cb) {
       if constexpr (PARITY) {
@@ -103,15 +103,15 @@ __device__ __forceinline__ unsigned long long f2fma(unsigned long long a, unsign
 
 template <int RB, int CB, int KS>
 __device__ __forceinline__ void mac4_x2(unsigned long long (&acc)[RB][CB][2], const float* Es,
-                                        const float* Hs, int tid, int k4,
+                                        const float* Hs, int rbase, int cbase, int cstride, int k4,
                                         unsigned long long negz, unsigned long long one) {
   ulonglong2 e[CB];
 #pragma unroll
   for (int cb = 0; cb < CB; ++cb)
-    e[cb] = *reinterpret_cast<const ulonglong2*>(Es + (tid + cb * kLT) * KS + k4 * 4);
+    e[cb] = *reinterpret_cast<const ulonglong2*>(Es + (cbase + cb * cstride) * KS + k4 * 4);
 #pragma unroll
   for (int rb = 0; rb < RB; ++rb) {
-    const ulonglong2 h = *reinterpret_cast<const ulonglong2*>(Hs + rb * KS + k4 * 4);
+    const ulonglong2 h = *reinterpret_cast<const ulonglong2*>(Hs + (rbase + rb) * KS + k4 * 4);
 #pragma unroll
     for (int cb = 0; cb < CB; ++cb) {
       acc[rb][cb][0] = f2fma(acc[rb][cb][0], one, f2fma(h.x, e[cb].x, negz));
@@ -120,7 +120,12 @@ __device__ __forceinline__ void mac4_x2(unsigned long long (&acc)[RB][CB][2], co
   }
 }
 
-template <int RB, int CB, bool PARITY, bool VEC, int kStages, int KC>
+// TWO_D: a warp owns all RB rows x 8 TC columns as a 4 x 8 lane grid, each
+// lane RB/4 rows x TC columns (stride 8): its H loads are shared by the 8
+// lanes of a row group and its E loads by the 4 of a column group, so one
+// 16-byte LDS is a single wavefront (vs 4 for 32 distinct E rows) and a
+// thread issues RB/4 + TC loads per 4-step instead of RB + 1.
+template <int RB, int CB, bool PARITY, bool VEC, int kStages, int KC, bool TWO_D = false>
 __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs a) {
   constexpr int kKC = KC;
   constexpr int kKS = KC + 4;
@@ -132,6 +137,12 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
   constexpr int NA = PARITY ? 4 : 1;
   uint32_t* sid = reinterpret_cast<uint32_t*>(sm + kStages * STAGE);
   const int tid = threadIdx.x, warp = tid >> 5;
+  static_assert(!TWO_D || (RB % 4 == 0 && CT % 32 == 0), "2-D tile: RB = 4 TR, CT = 32 TC");
+  constexpr int TR = TWO_D ? RB / 4 : RB;  // rows per thread
+  constexpr int TC = TWO_D ? CT / 32 : CB;  // columns per thread
+  const int rbase = TWO_D ? ((tid & 31) >> 3) * TR : 0;
+  const int cbase = TWO_D ? warp * (8 * TC) + (tid & 7) : tid;
+  constexpr int cstride = TWO_D ? 8 : kLT;
   const int d = a.d;
   const int d4 = d & ~3;
   const int nchunks = (d + kKC - 1) / kKC;
@@ -219,20 +230,20 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
       }
     };
 
-    float acc[RB][CB][NA];
+    float acc[TR][TC][NA];
 #pragma unroll
-    for (int rb = 0; rb < RB; ++rb)
+    for (int rb = 0; rb < TR; ++rb)
 #pragma unroll
-      for (int cb = 0; cb < CB; ++cb)
+      for (int cb = 0; cb < TC; ++cb)
 #pragma unroll
         for (int k = 0; k < NA; ++k) acc[rb][cb][k] = 0.0f;
     constexpr bool X2 = PARITY && VEC;  // paired FP32 path (see mac4_x2)
-    unsigned long long acc2[X2 ? RB : 1][X2 ? CB : 1][2];
+    unsigned long long acc2[X2 ? TR : 1][X2 ? TC : 1][2];
     if constexpr (X2) {
 #pragma unroll
-      for (int rb = 0; rb < RB; ++rb)
+      for (int rb = 0; rb < TR; ++rb)
 #pragma unroll
-        for (int cb = 0; cb < CB; ++cb) acc2[rb][cb][0] = acc2[rb][cb][1] = 0ull;
+        for (int cb = 0; cb < TC; ++cb) acc2[rb][cb][0] = acc2[rb][cb][1] = 0ull;
     }
 
 #pragma unroll
@@ -241,7 +252,7 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
       cp_async_commit();
     }
     // a warp whose 32 columns are all past the tile end skips the math
-    const bool warp_live = warp * 32 < ncols;
+    const bool warp_live = (TWO_D ? warp * 8 * TC : warp * 32) < ncols;
     for (int kc = 0; kc < nchunks; ++kc) {
       cp_async_wait<kStages - 2>();
       __syncthreads();
@@ -254,43 +265,40 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
       const float* Hs = Es + CT * kKS;
       const int kv = max(0, min(kKC, d4 - kc * kKC)) >> 2;  // full 4-lane groups
       if (warp_live) {
-        bool done = false;
         if constexpr (X2) {
-          if (a.use_x2) {
-            done = true;
-            if (kv == kKC / 4) {
-#pragma unroll
-            for (int k4 = 0; k4 < kKC / 4; ++k4)
-                mac4_x2<RB, CB, kKS>(acc2, Es, Hs, tid, k4, a.x2_negzero, a.x2_one);
-            } else {
-              for (int k4 = 0; k4 < kv; ++k4)
-                mac4_x2<RB, CB, kKS>(acc2, Es, Hs, tid, k4, a.x2_negzero, a.x2_one);
-            }
-          }
-        }
-        if (!done) {
           if (kv == kKC / 4) {
 #pragma unroll
-            for (int k4 = 0; k4 < kKC / 4; ++k4) mac4<RB, CB, PARITY, kKS>(acc, Es, Hs, tid, k4);
+            for (int k4 = 0; k4 < kKC / 4; ++k4)
+              mac4_x2<TR, TC, kKS>(acc2, Es, Hs, rbase, cbase, cstride, k4, a.x2_negzero,
+                                   a.x2_one);
           } else {
-            for (int k4 = 0; k4 < kv; ++k4) mac4<RB, CB, PARITY, kKS>(acc, Es, Hs, tid, k4);
+            for (int k4 = 0; k4 < kv; ++k4)
+              mac4_x2<TR, TC, kKS>(acc2, Es, Hs, rbase, cbase, cstride, k4, a.x2_negzero,
+                                   a.x2_one);
+          }
+        } else {
+          if (kv == kKC / 4) {
+#pragma unroll
+            for (int k4 = 0; k4 < kKC / 4; ++k4)
+              mac4<TR, TC, PARITY, kKS>(acc, Es, Hs, rbase, cbase, cstride, k4);
+          } else {
+            for (int k4 = 0; k4 < kv; ++k4)
+              mac4<TR, TC, PARITY, kKS>(acc, Es, Hs, rbase, cbase, cstride, k4);
           }
         }
       }
     }
     cp_async_wait<0>();
-    if constexpr (X2) {
-      if (a.use_x2) {  // unpack the pairs into the four reference lanes
+    if constexpr (X2) {  // unpack the pairs into the four reference lanes
 #pragma unroll
-      for (int rb = 0; rb < RB; ++rb)
+      for (int rb = 0; rb < TR; ++rb)
 #pragma unroll
-        for (int cb = 0; cb < CB; ++cb) {
+        for (int cb = 0; cb < TC; ++cb) {
           acc[rb][cb][0] = __uint_as_float(static_cast<uint32_t>(acc2[rb][cb][0]));
           acc[rb][cb][1] = __uint_as_float(static_cast<uint32_t>(acc2[rb][cb][0] >> 32));
           acc[rb][cb][2] = __uint_as_float(static_cast<uint32_t>(acc2[rb][cb][1]));
           acc[rb][cb][3] = __uint_as_float(static_cast<uint32_t>(acc2[rb][cb][1] >> 32));
         }
-      }
     }
     // the d mod 4 tail (all of d when d < 4) sits in the last chunk: lane 0
     if (d4 < d && warp_live) {
@@ -299,11 +307,11 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
       const float* Hs = Es + CT * kKS;
       for (int k = d4; k < d; ++k) {
 #pragma unroll
-        for (int rb = 0; rb < RB; ++rb) {
-          const float h = Hs[rb * kKS + k - cl];
+        for (int rb = 0; rb < TR; ++rb) {
+          const float h = Hs[(rbase + rb) * kKS + k - cl];
 #pragma unroll
-          for (int cb = 0; cb < CB; ++cb) {
-            const float e = Es[(tid + cb * kLT) * kKS + k - cl];
+          for (int cb = 0; cb < TC; ++cb) {
+            const float e = Es[(cbase + cb * cstride) * kKS + k - cl];
             if (PARITY) acc[rb][cb][0] = __fadd_rn(__fmul_rn(h, e), acc[rb][cb][0]);
             else acc[rb][cb][0] = fmaf(h, e, acc[rb][cb][0]);
           }
@@ -311,15 +319,15 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
       }
     }
 #pragma unroll
-    for (int cb = 0; cb < CB; ++cb) {
-      const int c = tid + kLT * cb;
+    for (int cb = 0; cb < TC; ++cb) {
+      const int c = cbase + cstride * cb;
       if (c >= ncols) continue;
       const uint32_t wid = VEC ? sid[c] / static_cast<uint32_t>(d) : sid[c];  // VEC: sid = id*d
       const float bias = a.bias ? __ldg(a.bias + wid) : 0.0f;
       const size_t col = col0 + c;
 #pragma unroll
-      for (int rb = 0; rb < RB; ++rb) {
-        const int r = row0 + rb;
+      for (int rb = 0; rb < TR; ++rb) {
+        const int r = row0 + rbase + rb;
         if (r >= rowlim) continue;
         float v;
         if constexpr (PARITY) {
@@ -354,22 +362,22 @@ int choose_rb(int B) {
   return best;
 }
 
-template <int RB, int CB, bool PARITY, bool VEC, int NS, int KC = 32>
+template <int RB, int CB, bool PARITY, bool VEC, int NS, int KC = 32, bool TWO_D = false>
 static lsb_status launch_variant(lsb_ctx* ctx, const LogitsArgs& a, int grid) {
   constexpr size_t smem = logits_smem_bytes<RB, CB, NS, KC>();
   static bool configured = false;
+  auto* kern = k_logits<RB, CB, PARITY, VEC, NS, KC, TWO_D>;
   if (!configured) {
-    LSB_CUDA(cudaFuncSetAttribute(k_logits<RB, CB, PARITY, VEC, NS, KC>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+    LSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     configured = true;
   }
-  LSB_CUDA(launch_pdl(ctx, k_logits<RB, CB, PARITY, VEC, NS, KC>, dim3(grid), dim3(kLT), smem, a));
+  LSB_CUDA(launch_pdl(ctx, kern, dim3(grid), dim3(kLT), smem, a));
   LSB_LAUNCHED(ctx, "k_logits");
   return LSB_OK;
 }
 
-template <int RB, int CB, bool PARITY, int KC = 32>
+template <int RB, int CB, bool PARITY, int KC = 32, bool TWO_D = false>
 static lsb_status launch_logits_rb(lsb_ctx* ctx, LogitsArgs a, int target) {
   constexpr int CT = kLT * CB;
   const int rgroups = (a.R_total + RB - 1) / RB;
@@ -390,10 +398,10 @@ static lsb_status launch_logits_rb(lsb_ctx* ctx, LogitsArgs a, int target) {
   // Survivor-only launches (the shared block went to the tensor cores) have
   // no other CTAs to hide their L2 latency behind: 3-stage ring instead of 2.
   if (a.skip_shared)
-    return vec ? launch_variant<RB, CB, PARITY, true, 3, KC>(ctx, a, grid)
-               : launch_variant<RB, CB, PARITY, false, 3, KC>(ctx, a, grid);
-  return vec ? launch_variant<RB, CB, PARITY, true, 2, KC>(ctx, a, grid)
-             : launch_variant<RB, CB, PARITY, false, 2, KC>(ctx, a, grid);
+    return vec ? launch_variant<RB, CB, PARITY, true, 3, KC, TWO_D>(ctx, a, grid)
+               : launch_variant<RB, CB, PARITY, false, 3, KC, TWO_D>(ctx, a, grid);
+  return vec ? launch_variant<RB, CB, PARITY, true, 2, KC, TWO_D>(ctx, a, grid)
+             : launch_variant<RB, CB, PARITY, false, 2, KC, TWO_D>(ctx, a, grid);
 }
 
 // One column per thread, RB rows: 8 FP instructions (PARITY) or 4 FFMA
@@ -402,8 +410,6 @@ lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_c
   const bool fast = mode == LSB_MODE_FAST;
   a.x2_negzero = 0x8000000080000000ull;  // runtime operands of the paired FP32 path
   a.x2_one = 0x3F8000003F800000ull;
-  static const bool no_x2 = getenv("LSB_NO_X2") != nullptr;
-  a.use_x2 = no_x2 ? 0 : 1;
   // FAST + enough rows sharing the identity columns [0, n_shared): a dense
   // contraction -> tcgen05 tensor cores; the per-sentence survivors stay on
   // the FFMA kernel below.
@@ -430,11 +436,19 @@ lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_c
   // (A 6-row x 2-column tile with 16-float chunks halves the H loads per
   // FFMA2 but measured 151 us vs 121 us at cfg 2: more E-tile refills and
   // spills; the 12 x 1 tile stays.)
+  static const bool one_d = getenv("LSB_K4_1D") != nullptr;
+#define LSB_RB2(R)                                                                   \
+  case R:                                                                            \
+    if (!one_d)                                                                      \
+      return fast ? launch_logits_rb<R, 1, false, 32, true>(ctx, a, target_ctas)     \
+                  : launch_logits_rb<R, 1, true, 32, true>(ctx, a, target_ctas);     \
+    return fast ? launch_logits_rb<R, 1, false>(ctx, a, target_ctas)                 \
+                : launch_logits_rb<R, 1, true>(ctx, a, target_ctas);
   switch (choose_rb(a.Bsent)) {
-    LSB_RB(16)
-    LSB_RB(12)
+    LSB_RB2(16)
+    LSB_RB2(12)
     LSB_RB(10)
-    LSB_RB(8)
+    LSB_RB2(8)
     LSB_RB(6)
     LSB_RB(4)
     LSB_RB(2)
@@ -443,6 +457,7 @@ lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_c
                   : launch_logits_rb<1, 1, true>(ctx, a, target_ctas);
   }
 #undef LSB_RB
+#undef LSB_RB2
 }
 
 }  // namespace lsb

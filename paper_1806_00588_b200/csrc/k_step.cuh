@@ -65,7 +65,6 @@ struct LogitsArgs {
   float* tc_H;             // FAST: scratch for the per-step tiled H
   int tc_N;                // rows per tcgen05 tile the scratch was sized for
   unsigned long long x2_negzero, x2_one;  // (-0,-0) / (1,1) f32x2 operands, set by launch
-  int use_x2;              // PARITY: paired FP32 (FFMA2) inner loop
 };
 
 // K5a: row softmax + per-row top-B by (p desc, column asc).
