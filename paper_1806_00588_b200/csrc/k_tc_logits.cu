@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "async_copy.cuh"
 #include "k_step.cuh"
 
 namespace lsb {
@@ -38,10 +39,6 @@ namespace tc {
 constexpr int kM = 128;        // candidate columns per CTA (UMMA M)
 constexpr int kKC = 32;        // d per chunk
 constexpr int kThreads = 128;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 
 // Canonical K-major, no-swizzle UMMA shared-memory descriptor: 8-row x 16-B
 // core matrices, rows 16 B apart; the next 8 rows SBO bytes away, the next
@@ -75,35 +72,6 @@ __device__ __forceinline__ void mma_commit(uint64_t* mbar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
           smem_u32(mbar)));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(mbar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(mbar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred done;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
-      "@!done bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
-      "r"(parity)
-      : "memory");
-}
-
-// TMA bulk copy global -> shared, completion counted on mbar (bytes % 16 == 0)
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(mbar))
-      : "memory");
 }
 
 __device__ __forceinline__ float tf32_rna(float x) {
