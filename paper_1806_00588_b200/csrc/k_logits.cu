@@ -50,9 +50,17 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-template <int RB, int CB, int NS, int KC>
+// columns per CTA tile: CB per thread, one per thread-column (1-D: 128
+// threads) or 8 per warp (2-D: 4 warps)
+template <int CB, bool TWO_D>
+constexpr int tile_cols() {
+  return TWO_D ? 32 * CB : kLT * CB;
+}
+
+template <int RB, int CB, int NS, int KC, bool TWO_D = false>
 constexpr size_t logits_smem_bytes() {
-  return static_cast<size_t>(NS) * (kLT * CB + RB) * (KC + 4) * 4 + kLT * CB * 4;
+  constexpr int CT = tile_cols<CB, TWO_D>();
+  return static_cast<size_t>(NS) * (CT + RB) * (KC + 4) * 4 + CT * 4;
 }
 
 // One 4-wide step of d for RB rows x CB columns: float4 of H (smem
@@ -132,14 +140,15 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
   constexpr int kParts = KC / 4;           // 16-byte pieces per row chunk
   constexpr int kRowStep = kLT / kParts;   // rows covered by one pass of the CTA
   extern __shared__ __align__(16) float sm[];
-  constexpr int CT = kLT * CB;
+  constexpr int CT = tile_cols<CB, TWO_D>();
   constexpr int STAGE = (CT + RB) * kKS;
   constexpr int NA = PARITY ? 4 : 1;
   uint32_t* sid = reinterpret_cast<uint32_t*>(sm + kStages * STAGE);
   const int tid = threadIdx.x, warp = tid >> 5;
-  static_assert(!TWO_D || (RB % 4 == 0 && CT % 32 == 0), "2-D tile: RB = 4 TR, CT = 32 TC");
+  static_assert(!TWO_D || RB % 4 == 0, "2-D tile: RB = 4 TR");
+  static_assert(CT % (kLT / (KC / 4)) == 0, "whole 16-byte pieces per loader thread");
   constexpr int TR = TWO_D ? RB / 4 : RB;  // rows per thread
-  constexpr int TC = TWO_D ? CT / 32 : CB;  // columns per thread
+  constexpr int TC = CB;                   // columns per thread
   const int rbase = TWO_D ? ((tid & 31) >> 3) * TR : 0;
   const int cbase = TWO_D ? warp * (8 * TC) + (tid & 7) : tid;
   constexpr int cstride = TWO_D ? 8 : kLT;
@@ -364,7 +373,7 @@ int choose_rb(int B) {
 
 template <int RB, int CB, bool PARITY, bool VEC, int NS, int KC = 32, bool TWO_D = false>
 static lsb_status launch_variant(lsb_ctx* ctx, const LogitsArgs& a, int grid) {
-  constexpr size_t smem = logits_smem_bytes<RB, CB, NS, KC>();
+  constexpr size_t smem = logits_smem_bytes<RB, CB, NS, KC, TWO_D>();
   static bool configured = false;
   auto* kern = k_logits<RB, CB, PARITY, VEC, NS, KC, TWO_D>;
   if (!configured) {
@@ -379,7 +388,7 @@ static lsb_status launch_variant(lsb_ctx* ctx, const LogitsArgs& a, int grid) {
 
 template <int RB, int CB, bool PARITY, int KC = 32, bool TWO_D = false>
 static lsb_status launch_logits_rb(lsb_ctx* ctx, LogitsArgs a, int target) {
-  constexpr int CT = kLT * CB;
+  constexpr int CT = tile_cols<CB, TWO_D>();
   const int rgroups = (a.R_total + RB - 1) / RB;
   a.ctiles_shared = static_cast<int>((a.n_shared + CT - 1) / CT);
   a.jobs_shared = (a.n_shared && !a.skip_shared) ? rgroups * a.ctiles_shared : 0;
@@ -433,15 +442,16 @@ lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_c
   case R:                                                                \
     return fast ? launch_logits_rb<R, 1, false>(ctx, a, target_ctas)     \
                 : launch_logits_rb<R, 1, true>(ctx, a, target_ctas);
-  // (A 6-row x 2-column tile with 16-float chunks halves the H loads per
-  // FFMA2 but measured 151 us vs 121 us at cfg 2: more E-tile refills and
-  // spills; the 12 x 1 tile stays.)
+  // Measured at cfg 2 (PARITY, B200): 1-D 12x1 tile 119 us; 2-D 3x4 per
+  // lane 100 us; 2-D 3x3 106 us; 2-D with 64- or 256-thread CTAs 115 / 165
+  // us; 1-D 6x2 with 16-float chunks 151 us; 4 CTAs/SM at 128 registers
+  // 116 us; TMA bulk row copies 129 us (the per-lane operands serialise).
   static const bool one_d = getenv("LSB_K4_1D") != nullptr;
 #define LSB_RB2(R)                                                                   \
   case R:                                                                            \
     if (!one_d)                                                                      \
-      return fast ? launch_logits_rb<R, 1, false, 32, true>(ctx, a, target_ctas)     \
-                  : launch_logits_rb<R, 1, true, 32, true>(ctx, a, target_ctas);     \
+      return fast ? launch_logits_rb<R, 4, false, 32, true>(ctx, a, target_ctas)     \
+                  : launch_logits_rb<R, 4, true, 32, true>(ctx, a, target_ctas);     \
     return fast ? launch_logits_rb<R, 1, false>(ctx, a, target_ctas)                 \
                 : launch_logits_rb<R, 1, true>(ctx, a, target_ctas);
   switch (choose_rb(a.Bsent)) {
