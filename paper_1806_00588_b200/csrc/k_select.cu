@@ -52,8 +52,8 @@ __device__ __forceinline__ T block_reduce(T v, T* red, Op op) {
 // round trips through L2 -- and the top-B is B rounds of a block-wide
 // arg-max by (p desc, column asc) in which only the owner of the winning
 // column rescans its registers. Same arithmetic as the general path.
-constexpr int kSelReg = 16;
-constexpr int kSelCand = 128;  // threshold survivors ranked directly
+constexpr int kSelReg = 24;
+constexpr int kSelCand = 256;  // threshold survivors ranked directly
 
 __device__ __forceinline__ void row_registers(const SoftmaxArgs& a, int row, float* L, uint32_t n,
                                               float* red_f, double* red_d) {
@@ -99,61 +99,78 @@ __device__ __forceinline__ void row_registers(const SoftmaxArgs& a, int row, flo
       v[k] = -1.0f;
     }
   }
-  // Threshold filter: per warp, the B-th largest of the 32 lane maxima (a
-  // shuffle bitonic sort) is a lower bound for the row's B-th largest p, so
-  // is the maximum of those bounds over the warps; only entries >= it can be
-  // in the top-B. Usually a few dozen survive: rank them exactly in one warp.
+  // Threshold filter: tau = the B-th largest of the kSelT lane maxima (each
+  // warp sorts its 32 with a shuffle bitonic network, every lane ranks its
+  // value against the other warps' sorted lists) is a lower bound for the
+  // row's B-th largest p -- B lanes hold an entry >= tau -- so only entries
+  // >= tau can be in the top-B. Usually a few dozen survive; all threads rank
+  // them exactly by (p desc, column asc).
   {
-    __shared__ float s_tau[kSelT / 32];
+    __shared__ float s_lm[kSelT];
+    __shared__ float s_tau;
     __shared__ int s_nc;
     __shared__ float c_p[kSelCand];
     __shared__ uint32_t c_c[kSelCand];
-    float tm = -1.0f;
+    float x = -1.0f;
 #pragma unroll
-    for (int k = 0; k < kSelReg; ++k) tm = fmaxf(tm, v[k]);
-    float x = tm;  // bitonic sort of the warp's 32 lane maxima, descending
+    for (int k = 0; k < kSelReg; ++k) x = fmaxf(x, v[k]);
 #pragma unroll
-    for (int size = 2; size <= 32; size <<= 1)
+    for (int size = 2; size <= 32; size <<= 1)  // bitonic sort, descending
 #pragma unroll
       for (int stride = size >> 1; stride > 0; stride >>= 1) {
         const float y = __shfl_xor_sync(0xffffffffu, x, stride);
         const bool up = ((lane & size) == 0) == ((lane & stride) == 0);
         x = up ? fmaxf(x, y) : fminf(x, y);
       }
-    const int bsel = min(a.topB, 32);
-    const float tau_w = __shfl_sync(0xffffffffu, x, bsel - 1);
-    if (lane == 0) s_tau[warp] = a.topB <= 32 ? tau_w : -1.0f;
-    if (tid == 0) s_nc = 0;
-    __syncthreads();
-    float tau = s_tau[0];
-#pragma unroll
-    for (int w = 1; w < kSelT / 32; ++w) tau = fmaxf(tau, s_tau[w]);
-    if (tau >= 0.0f) {
-#pragma unroll
-      for (int k = 0; k < kSelReg; ++k)
-        if (v[k] >= tau) {
-          const int at = atomicAdd(&s_nc, 1);
-          if (at < kSelCand) {
-            c_p[at] = v[k];
-            c_c[at] = tid + kSelT * k;
-          }
-        }
+    s_lm[tid] = x;
+    if (tid == 0) {
+      s_tau = -1.0f;
+      s_nc = 0;
     }
     __syncthreads();
-    const int nc = s_nc;
-    const int keep = static_cast<int>(min(static_cast<uint32_t>(a.topB), n));
-    if (tau >= 0.0f && nc <= kSelCand && nc >= keep) {
-      if (warp == 0) {
-        TopEntry* out = a.top + static_cast<size_t>(row) * a.topB;
-        for (int q = lane; q < nc; q += 32) {
-          const float p = c_p[q];
-          const uint32_t c = c_c[q];
-          int rank = 0;
-          for (int j = 0; j < nc; ++j) rank += top_better(c_p[j], c_c[j], p, c);
-          if (rank < keep) out[rank] = TopEntry{p, c};
+    const int K = B;
+    if (K <= kSelT) {
+      // rank in (value desc, list position asc) order: unique ranks 0..kSelT-1
+      int rank = lane;
+#pragma unroll
+      for (int w = 0; w < kSelT / 32; ++w) {
+        if (w == warp) continue;
+        const float* l = s_lm + w * 32;
+        int lo = 0, hi = 32;  // count of l[] before me: > x, or >= x for earlier warps
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          const bool before = w < warp ? l[mid] >= x : l[mid] > x;
+          if (before) lo = mid + 1;
+          else hi = mid;
         }
-        if (lane == 0) a.top_n[row] = keep;
+        rank += lo;
       }
+      if (rank == K - 1) s_tau = x;
+    }
+    __syncthreads();
+    const float tau = fmaxf(s_tau, 0.0f);  // valid entries are >= 0, padding -1
+#pragma unroll
+    for (int k = 0; k < kSelReg; ++k)
+      if (v[k] >= tau) {
+        const int at = atomicAdd(&s_nc, 1);
+        if (at < kSelCand) {
+          c_p[at] = v[k];
+          c_c[at] = tid + kSelT * k;
+        }
+      }
+    __syncthreads();
+    const int nc = s_nc;
+    const int keep = static_cast<int>(min(static_cast<uint32_t>(B), n));
+    if (nc <= kSelCand) {
+      TopEntry* out = a.top + static_cast<size_t>(row) * B;
+      for (int q = tid; q < nc; q += kSelT) {
+        const float p = c_p[q];
+        const uint32_t c = c_c[q];
+        int rank = 0;
+        for (int j = 0; j < nc; ++j) rank += top_better(c_p[j], c_c[j], p, c);
+        if (rank < keep) out[rank] = TopEntry{p, c};
+      }
+      if (tid == 0) a.top_n[row] = keep;
       return;
     }
     // (many ties at the threshold: fall through to the round-based merge)
@@ -428,6 +445,9 @@ __global__ void __launch_bounds__(kExpT) k_expand(ExpandArgs a) {
   uint32_t* cb = reinterpret_cast<uint32_t*>(cw + cap);
   int* co = reinterpret_cast<int*>(cb + cap);  // own list of each candidate
   int* cr = co + cap;                          // rank accumulators
+  int* surv = cr + cap;                        // candidates left after pruning
+  __shared__ int s_heads[kRankMaxLists];       // list heads, best first
+  __shared__ int s_nh, s_nsurv;
 
   // list lengths -> offsets (nl <= kRankMaxLists: one warp scans)
   if (threadIdx.x < 32) {
@@ -491,11 +511,55 @@ __global__ void __launch_bounds__(kExpT) k_expand(ExpandArgs a) {
     cr[e] = j;  // position in its own list
   }
   __syncthreads();
+  // Pruning (large beams): a candidate at position j of its list is beaten
+  // by its j predecessors and by every other list's head that beats it, so
+  // j + #(better foreign heads) >= B rules it out of the top-B without its
+  // nl binary searches; heads are ranked once (nl <= kRankMaxLists).
+  const int B = a.topB;
+  int nsurv = total;
+  const bool prune = B > 16;
+  if (prune) {
+    if (threadIdx.x == 0) {
+      s_nh = 0;
+      s_nsurv = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x < nl && s_off[threadIdx.x] < s_off[threadIdx.x + 1]) {
+      const int eh = s_off[threadIdx.x];
+      const Cand me{cs[eh], cb[eh], cw[eh]};
+      int rank = 0;
+      for (int l = 0; l < nl; ++l) {
+        const int o = s_off[l];
+        if (l != static_cast<int>(threadIdx.x) && o < s_off[l + 1] &&
+            cand_better(Cand{cs[o], cb[o], cw[o]}, me))
+          ++rank;
+      }
+      s_heads[rank] = eh;
+      atomicAdd(&s_nh, 1);
+    }
+    __syncthreads();
+    const int nh = s_nh;
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      const Cand me{cs[e], cb[e], cw[e]};
+      int lo = 0, hi = nh;  // heads better than me (includes my own when j > 0)
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const int h = s_heads[mid];
+        if (cand_better(Cand{cs[h], cb[h], cw[h]}, me)) lo = mid + 1;
+        else hi = mid;
+      }
+      const int j = cr[e];
+      if (j + lo - (j > 0 ? 1 : 0) < B) surv[atomicAdd(&s_nsurv, 1)] = e;
+      else cr[e] = 0x3FFFFFFF;  // rank >= B: never written out
+    }
+    __syncthreads();
+    nsurv = s_nsurv;
+  }
   // rank = own position + per other list the count of better entries; one
   // (candidate, list) pair per thread so the binary searches run in parallel
-  const int B = a.topB;
-  for (int q = threadIdx.x; q < total * nl; q += blockDim.x) {
-    const int e = q / nl, l = q - e * nl;
+  for (int q = threadIdx.x; q < nsurv * nl; q += blockDim.x) {
+    const int qe = q / nl, l = q - qe * nl;
+    const int e = prune ? surv[qe] : qe;
     if (l == co[e] || s_off[l] == s_off[l + 1]) continue;
     const Cand me{cs[e], cb[e], cw[e]};
     int b0 = s_off[l], b1 = s_off[l + 1];  // first entry of l not better than me
@@ -936,7 +1000,7 @@ lsb_status launch_select_fused(lsb_ctx* ctx, const SoftmaxArgs& sa, const Expand
 lsb_status launch_expand(lsb_ctx* ctx, const ExpandArgs& a) {
   if (a.S == 0) return LSB_OK;
   const int nl = (a.frozen_mode ? a.nfrozen : 0) + a.Bsent;
-  const size_t rank_smem = static_cast<size_t>(nl) * std::max(a.topB, 1) * (8 + 8 + 4 + 4 + 4);
+  const size_t rank_smem = static_cast<size_t>(nl) * std::max(a.topB, 1) * (8 + 8 + 4 + 4 + 4 + 4);
   if (nl <= kRankMaxLists && rank_smem <= ctx->smem_optin) {
     static size_t configured = 0;
     if (rank_smem > configured) {

@@ -52,7 +52,10 @@ def time_steps(ctx, step, n_inputs, steps=50, warmup=3):
     for k in range(warmup):
         step(k % n_inputs)
     ctx.sync()
-    st = torch.cuda.ExternalStream(ctx.stream)
+    # the context runs on torch's stream (handle 0 is mapped to the legacy
+    # default stream, reported as 1)
+    st = (torch.cuda.current_stream() if ctx.stream in (0, 1)
+          else torch.cuda.ExternalStream(ctx.stream))
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(st)
     for k in range(steps):

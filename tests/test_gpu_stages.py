@@ -232,13 +232,17 @@ def test_softmax_examples(ctx):
         ctx.softmax_rows(np.full((1, 3), -np.inf, np.float32))
 
 
-@pytest.mark.parametrize("rows,n,B,nfz", [(12, 1335, 12, 0), (4, 50, 3, 2), (1, 4, 1, 0),
-                                          (2, 3, 3, 0), (5, 100, 12, 3), (50, 300, 50, 0)])
-def test_expand_beams_parity(ctx, oracle, rows, n, B, nfz):
+@pytest.mark.parametrize("rows,n,B,nfz,ties", [
+    (12, 1335, 12, 0, False), (4, 50, 3, 2, False), (1, 4, 1, 0, False), (2, 3, 3, 0, False),
+    (5, 100, 12, 3, False), (50, 300, 50, 0, False), (30, 200, 40, 5, False),
+    (20, 64, 24, 2, True), (50, 50, 50, 0, True)])
+def test_expand_beams_parity(ctx, oracle, rows, n, B, nfz, ties):
     rng = np.random.default_rng(rows * 100 + n)
     logits = rng.standard_normal((rows, n)).astype(np.float32) * 2
+    if ties:  # equal scores everywhere: order decided by (beam, word) alone
+        logits[:] = 0.0
     probs = oracle.softmax_rows(logits)
-    cum = -rng.random(rows) * 3
+    cum = np.zeros(rows) if ties else -rng.random(rows) * 3
     live = np.arange(nfz, nfz + rows, dtype=np.uint32)
     frozen = [(-rng.random() * 2, i) for i in range(nfz)]
     id_map = np.sort(rng.choice(10 * n, n, replace=False)).astype(np.uint32)

@@ -55,6 +55,10 @@ CASES = [
     (2000, 64, 8, 3, 100, 2, 12, 0, 0),
     (5000, 1003, 16, 3, 32, 2, 7, 50, 1),
     (1500, 256, 16, 3, 300, 2, 12, 25, 5),
+    # large beams: K5a threshold over 128 lane maxima (B > 32), rows of
+    # > 2048 candidates in registers, K5b head pruning (B > 16)
+    (6000, 64, 8, 3, 16, 2, 50, 2200, 2),
+    (4000, 64, 4, 2, 8, 2, 24, 100, 1),
 ]
 
 
