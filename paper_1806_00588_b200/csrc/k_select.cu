@@ -47,6 +47,61 @@ __device__ __forceinline__ T block_reduce(T v, T* red, Op op) {
   return v;
 }
 
+// The K-th largest of the CTA's kSelT per-thread values x (-1 = none): each
+// warp sorts its 32 with a shuffle bitonic network, every lane ranks its value
+// against the other warps' sorted lists in (value desc, position asc) order.
+// K lanes hold an entry >= the result, so it bounds the row's K-th largest
+// from below. Returns -1 when K > kSelT. Contains barriers (whole CTA).
+__device__ __forceinline__ float kth_lane_max(float x, int K) {
+  __shared__ float s_lm[kSelT];
+  __shared__ float s_tau;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1)  // bitonic sort, descending
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const float y = __shfl_xor_sync(0xffffffffu, x, stride);
+      const bool up = ((lane & size) == 0) == ((lane & stride) == 0);
+      x = up ? fmaxf(x, y) : fminf(x, y);
+    }
+  if (K <= 32) {
+    // cheaper, looser bound: each warp's K-th largest (K lanes of that warp
+    // hold an entry >= it), maximised over the warps
+    const float kw = __shfl_sync(0xffffffffu, x, K - 1);
+    if (lane == 0) s_lm[warp] = kw;
+    __syncthreads();
+    float t = s_lm[0];
+#pragma unroll
+    for (int w = 1; w < kSelT / 32; ++w) t = fmaxf(t, s_lm[w]);
+    __syncthreads();  // s_lm may be reused by the next call
+    return t;
+  }
+  s_lm[tid] = x;
+  if (tid == 0) s_tau = -1.0f;
+  __syncthreads();
+  if (K <= kSelT) {
+    int rank = lane;
+#pragma unroll
+    for (int w = 0; w < kSelT / 32; ++w) {
+      if (w == warp) continue;
+      const float* l = s_lm + w * 32;
+      int lo = 0, hi = 32;  // entries of l before me: > x, or >= x for earlier warps
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const bool before = w < warp ? l[mid] >= x : l[mid] > x;
+        if (before) lo = mid + 1;
+        else hi = mid;
+      }
+      rank += lo;
+    }
+    if (rank == K - 1) s_tau = x;
+  }
+  __syncthreads();
+  const float t = s_tau;
+  __syncthreads();  // s_lm / s_tau may be reused by the next call
+  return t;
+}
+
 // Rows of at most kSelT * kSelReg candidates (the LSH step's): the row lives
 // in registers, kSelReg values per thread -- one global read, no exp/prob
 // round trips through L2 -- and the top-B is B rounds of a block-wide
@@ -55,16 +110,17 @@ __device__ __forceinline__ T block_reduce(T v, T* red, Op op) {
 constexpr int kSelReg = 24;
 constexpr int kSelCand = 256;  // threshold survivors ranked directly
 
+template <int REG>
 __device__ __forceinline__ void row_registers(const SoftmaxArgs& a, int row, float* L, uint32_t n,
                                               float* red_f, double* red_d) {
   __shared__ float win_p[2][kSelT / 32];
   __shared__ uint32_t win_r[2][kSelT / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int B = a.topB;
-  float v[kSelReg];
+  float v[REG];
   float mx = -INFINITY;
 #pragma unroll
-  for (int k = 0; k < kSelReg; ++k) {
+  for (int k = 0; k < REG; ++k) {
     const uint32_t c = tid + kSelT * k;
     v[k] = c < n ? L[c] : -INFINITY;
     mx = (mx < v[k]) ? v[k] : mx;
@@ -80,7 +136,7 @@ __device__ __forceinline__ void row_registers(const SoftmaxArgs& a, int row, flo
   const double dmx = static_cast<double>(mx);
   double sum = 0.0;
 #pragma unroll
-  for (int k = 0; k < kSelReg; ++k) {
+  for (int k = 0; k < REG; ++k) {
     if (tid + kSelT * k < n) {
       const double e = exp(static_cast<double>(v[k]) - dmx);
       v[k] = static_cast<float>(e);
@@ -90,7 +146,7 @@ __device__ __forceinline__ void row_registers(const SoftmaxArgs& a, int row, flo
   sum = block_reduce(sum, red_d, [](double x, double y) { return x + y; });
   const float inv = static_cast<float>(1.0 / sum);
 #pragma unroll
-  for (int k = 0; k < kSelReg; ++k) {
+  for (int k = 0; k < REG; ++k) {
     const uint32_t c = tid + kSelT * k;
     if (c < n) {
       v[k] = __fmul_rn(v[k], inv);
@@ -99,58 +155,21 @@ __device__ __forceinline__ void row_registers(const SoftmaxArgs& a, int row, flo
       v[k] = -1.0f;
     }
   }
-  // Threshold filter: tau = the B-th largest of the kSelT lane maxima (each
-  // warp sorts its 32 with a shuffle bitonic network, every lane ranks its
-  // value against the other warps' sorted lists) is a lower bound for the
-  // row's B-th largest p -- B lanes hold an entry >= tau -- so only entries
-  // >= tau can be in the top-B. Usually a few dozen survive; all threads rank
-  // them exactly by (p desc, column asc).
+  // Threshold filter: only entries >= tau (the B-th largest lane maximum,
+  // kth_lane_max) can be in the top-B. Usually a few dozen survive; all
+  // threads rank them exactly by (p desc, column asc).
   {
-    __shared__ float s_lm[kSelT];
-    __shared__ float s_tau;
     __shared__ int s_nc;
     __shared__ float c_p[kSelCand];
     __shared__ uint32_t c_c[kSelCand];
     float x = -1.0f;
 #pragma unroll
-    for (int k = 0; k < kSelReg; ++k) x = fmaxf(x, v[k]);
+    for (int k = 0; k < REG; ++k) x = fmaxf(x, v[k]);
+    if (tid == 0) s_nc = 0;  // published by kth_lane_max's barriers
+    const float tau_k = kth_lane_max(x, B);
+    const float tau = fmaxf(tau_k, 0.0f);  // valid entries are >= 0, padding -1
 #pragma unroll
-    for (int size = 2; size <= 32; size <<= 1)  // bitonic sort, descending
-#pragma unroll
-      for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        const float y = __shfl_xor_sync(0xffffffffu, x, stride);
-        const bool up = ((lane & size) == 0) == ((lane & stride) == 0);
-        x = up ? fmaxf(x, y) : fminf(x, y);
-      }
-    s_lm[tid] = x;
-    if (tid == 0) {
-      s_tau = -1.0f;
-      s_nc = 0;
-    }
-    __syncthreads();
-    const int K = B;
-    if (K <= kSelT) {
-      // rank in (value desc, list position asc) order: unique ranks 0..kSelT-1
-      int rank = lane;
-#pragma unroll
-      for (int w = 0; w < kSelT / 32; ++w) {
-        if (w == warp) continue;
-        const float* l = s_lm + w * 32;
-        int lo = 0, hi = 32;  // count of l[] before me: > x, or >= x for earlier warps
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          const bool before = w < warp ? l[mid] >= x : l[mid] > x;
-          if (before) lo = mid + 1;
-          else hi = mid;
-        }
-        rank += lo;
-      }
-      if (rank == K - 1) s_tau = x;
-    }
-    __syncthreads();
-    const float tau = fmaxf(s_tau, 0.0f);  // valid entries are >= 0, padding -1
-#pragma unroll
-    for (int k = 0; k < kSelReg; ++k)
+    for (int k = 0; k < REG; ++k)
       if (v[k] >= tau) {
         const int at = atomicAdd(&s_nc, 1);
         if (at < kSelCand) {
@@ -178,7 +197,7 @@ __device__ __forceinline__ void row_registers(const SoftmaxArgs& a, int row, flo
   float bp = -1.0f;
   int bk = 0;
 #pragma unroll
-  for (int k = 0; k < kSelReg; ++k)
+  for (int k = 0; k < REG; ++k)
     if (v[k] > bp) {
       bp = v[k];
       bk = k;
@@ -212,12 +231,12 @@ __device__ __forceinline__ void row_registers(const SoftmaxArgs& a, int row, flo
     if (tid == 0) out[r] = TopEntry{p, c};
     if (c % kSelT == static_cast<uint32_t>(tid)) {  // the owner drops it and rescans
 #pragma unroll
-      for (int k = 0; k < kSelReg; ++k)
+      for (int k = 0; k < REG; ++k)
         if (k == bk) v[k] = -1.0f;
       bp = -1.0f;
       bk = 0;
 #pragma unroll
-      for (int k = 0; k < kSelReg; ++k)
+      for (int k = 0; k < REG; ++k)
         if (v[k] > bp) {
           bp = v[k];
           bk = k;
@@ -229,7 +248,6 @@ __device__ __forceinline__ void row_registers(const SoftmaxArgs& a, int row, flo
 
 // ===================================================================== K5a
 __global__ void __launch_bounds__(kSelT) k_softmax_topb(SoftmaxArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
   __shared__ float red_f[kSelT / 32];
   __shared__ double red_d[kSelT / 32];
   __shared__ float win_p[kSelT / 32];
@@ -247,7 +265,8 @@ __global__ void __launch_bounds__(kSelT) k_softmax_topb(SoftmaxArgs a) {
   const uint32_t n = a.n_cand ? a.n_cand[s] : a.n_const;
   float* L = a.logits + static_cast<size_t>(row) * a.ldl;
   if (!a.probs_in && n <= kSelT * kSelReg && B > 0) {
-    row_registers(a, row, L, n, red_f, red_d);
+    if (n <= kSelT * 16) row_registers<16>(a, row, L, n, red_f, red_d);
+    else row_registers<kSelReg>(a, row, L, n, red_f, red_d);
     return;
   }
   float inv = 1.0f;
@@ -280,29 +299,82 @@ __global__ void __launch_bounds__(kSelT) k_softmax_topb(SoftmaxArgs a) {
     if (tid == 0) a.top_n[row] = 0;
     return;
   }
-  // per-thread sorted lists, entry j of thread t at [j * kSelT + t]
-  float* lp = reinterpret_cast<float*>(smem);
-  uint32_t* lr = reinterpret_cast<uint32_t*>(lp + B * kSelT);
-  int cnt = 0;
+  // Rows longer than the register path (or probabilities given): the same
+  // threshold selection over global memory. Pass 1 forms p (written back when
+  // requested) and each thread's maximum; tau = the B-th largest of those
+  // maxima bounds the row's B-th largest p from below.
+  const bool pw = a.probs_in || a.keep_probs;  // L holds p after pass 1
+  auto p_at = [&](uint32_t r) { return pw ? L[r] : __fmul_rn(L[r], inv); };
+  float x = -1.0f;
   for (uint32_t r = tid; r < n; r += kSelT) {
     const float p = a.probs_in ? L[r] : __fmul_rn(L[r], inv);
     if (a.keep_probs && !a.probs_in) L[r] = p;
-    if (cnt == B && !(p > lp[(B - 1) * kSelT + tid])) continue;
-    int j = cnt < B ? cnt++ : B - 1;
-    while (j > 0 && lp[(j - 1) * kSelT + tid] < p) {
-      lp[j * kSelT + tid] = lp[(j - 1) * kSelT + tid];
-      lr[j * kSelT + tid] = lr[(j - 1) * kSelT + tid];
-      --j;
-    }
-    lp[j * kSelT + tid] = p;
-    lr[j * kSelT + tid] = r;
+    x = fmaxf(x, p);
   }
+  __shared__ int s_nc;
+  __shared__ float c_p[kSelCand];
+  __shared__ uint32_t c_c[kSelCand];
+  if (tid == 0) s_nc = 0;  // published by kth_lane_max's barriers
+  const float tau = kth_lane_max(x, B);
   const int keep = static_cast<int>(min(static_cast<uint32_t>(B), n));
   TopEntry* out = a.top + static_cast<size_t>(row) * B;
-  int head = 0;
+  // pass 2: survivors p >= tau (tau > 0), or every positive p (tau <= 0:
+  // fewer than B threads saw a positive p; zeros then fill by column)
+  for (uint32_t r = tid; r < n; r += kSelT) {
+    const float p = p_at(r);
+    if (tau > 0.0f ? p >= tau : p > 0.0f) {
+      const int at = atomicAdd(&s_nc, 1);
+      if (at < kSelCand) {
+        c_p[at] = p;
+        c_c[at] = r;
+      }
+    }
+  }
+  __syncthreads();
+  const int nc = s_nc;
+  if (nc <= kSelCand) {
+    for (int q = tid; q < nc; q += kSelT) {
+      const float p = c_p[q];
+      const uint32_t c = c_c[q];
+      int rank = 0;
+      for (int j = 0; j < nc; ++j) rank += top_better(c_p[j], c_c[j], p, c);
+      if (rank < keep) out[rank] = TopEntry{p, c};
+    }
+    // zeros, by ascending column, after every positive p
+    int filled = min(nc, keep);
+    for (uint32_t base = 0; filled < keep && base < n; base += kSelT) {
+      const uint32_t r = base + tid;
+      const bool z = r < n && !(p_at(r) > 0.0f);
+      const unsigned bal = __ballot_sync(0xffffffffu, z);
+      if (lane == 0) win_r[warp] = __popc(bal);
+      __syncthreads();
+      int before = 0, total = 0;
+#pragma unroll
+      for (int w = 0; w < kSelT / 32; ++w) {
+        before += w < warp ? static_cast<int>(win_r[w]) : 0;
+        total += static_cast<int>(win_r[w]);
+      }
+      const int pos = filled + before + __popc(bal & ((1u << lane) - 1u));
+      if (z && pos < keep) out[pos] = TopEntry{p_at(r), r};
+      filled += total;
+      __syncthreads();
+    }
+    if (tid == 0) a.top_n[row] = keep;
+    return;
+  }
+  // many ties at tau: keep rounds of a block-wide arg-max below the last key
+  float lp = INFINITY;
+  uint32_t lc = 0;
   for (int k = 0; k < keep; ++k) {
-    float bp = head < cnt ? lp[head * kSelT + tid] : -INFINITY;
-    uint32_t br = head < cnt ? lr[head * kSelT + tid] : 0xFFFFFFFFu;
+    float bp = -1.0f;
+    uint32_t br = 0xFFFFFFFFu;
+    for (uint32_t r = tid; r < n; r += kSelT) {
+      const float p = p_at(r);
+      if (top_better(lp, lc, p, r) && top_better(p, r, bp, br)) {
+        bp = p;
+        br = r;
+      }
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       const float yp = __shfl_xor_sync(0xffffffffu, bp, o);
@@ -323,8 +395,9 @@ __global__ void __launch_bounds__(kSelT) k_softmax_topb(SoftmaxArgs a) {
         bp = win_p[w];
         br = win_r[w];
       }
-    if ((br % kSelT) == static_cast<uint32_t>(tid)) ++head;
     if (tid == 0) out[k] = TopEntry{bp, br};
+    lp = bp;
+    lc = br;
     __syncthreads();
   }
   if (tid == 0) a.top_n[row] = keep;
@@ -332,15 +405,7 @@ __global__ void __launch_bounds__(kSelT) k_softmax_topb(SoftmaxArgs a) {
 
 lsb_status launch_softmax(lsb_ctx* ctx, const SoftmaxArgs& a) {
   if (a.R_total == 0) return LSB_OK;
-  const size_t smem = static_cast<size_t>(std::max(a.topB, 1)) * kSelT * 8;
-  if (smem > ctx->smem_optin) return set_error("softmax: beam too large"), LSB_EINVAL;
-  static size_t configured = 0;
-  if (smem > configured) {
-    LSB_CUDA(cudaFuncSetAttribute(k_softmax_topb, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    configured = smem;
-  }
-  LSB_CUDA(launch_pdl(ctx, k_softmax_topb, dim3(a.R_total), dim3(kSelT), smem, a));
+  LSB_CUDA(launch_pdl(ctx, k_softmax_topb, dim3(a.R_total), dim3(kSelT), 0, a));
   LSB_LAUNCHED(ctx, "k_softmax_topb");
   return LSB_OK;
 }

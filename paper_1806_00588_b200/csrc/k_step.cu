@@ -21,7 +21,10 @@
 namespace lsb {
 
 // =================================================================== K1+K2
-__global__ void __launch_bounds__(512) k_probe_count(ProbeArgs a) {
+constexpr int kWarpBands = 64;  // up to this many bands: a warp per band
+
+template <int NT>
+__global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(ProbeArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const IndexView& ix = a.ix;
   const int row = blockIdx.x;
@@ -42,7 +45,9 @@ __global__ void __launch_bounds__(512) k_probe_count(ProbeArgs a) {
   float* h = reinterpret_cast<float*>(smem + cbytes);
   const int dpad = (ix.d + 3) & ~3;
   uint32_t* codes = reinterpret_cast<uint32_t*>(h + dpad);
-  uint8_t* idx = reinterpret_cast<uint8_t*>(codes + ix.W);
+  uint32_t* sp_start = codes + ix.W;    // per band: span start (hit) ...
+  uint32_t* sp_pre = sp_start + ix.W;   // ... and exclusive prefix of span lengths [W + 1]
+  uint8_t* idx = reinterpret_cast<uint8_t*>(sp_pre + ix.W + 1);
 
   for (size_t k = threadIdx.x; k < cbytes / 16; k += blockDim.x)
     reinterpret_cast<uint4*>(cnt)[k] = make_uint4(0, 0, 0, 0);
@@ -91,19 +96,42 @@ __global__ void __launch_bounds__(512) k_probe_count(ProbeArgs a) {
       }
       idx[p_own] = static_cast<uint8_t>(best);
     }
-  } else
-  for (int p = threadIdx.x; p < ix.P; p += blockDim.x) {
-    const uint32_t* pr = ix.perms + static_cast<size_t>(p) * ix.K;
-    uint32_t best = 0;
-    float bv = h[__ldg(pr)];
-    for (int k = 1; k < ix.K; ++k) {
-      const float v = h[__ldg(pr + k)];
-      if (v > bv) {
-        bv = v;
-        best = k;
+  } else if (ix.K <= kMaxKReg) {
+    // more permutations than threads (large W): each thread's permutation
+    // rows are fetched whole (K loads in flight), not one load per step
+    for (int p = threadIdx.x; p < ix.P; p += blockDim.x) {
+      const uint32_t* pr = ix.perms + static_cast<size_t>(p) * ix.K;
+      uint32_t q[kMaxKReg];
+#pragma unroll
+      for (int k = 0; k < kMaxKReg; ++k) q[k] = k < ix.K ? __ldg(pr + k) : 0u;
+      uint32_t best = 0;
+      float bv = h[q[0]];
+#pragma unroll
+      for (int k = 1; k < kMaxKReg; ++k) {
+        if (k < ix.K) {
+          const float v = h[q[k]];
+          if (v > bv) {
+            bv = v;
+            best = k;
+          }
+        }
       }
+      idx[p] = static_cast<uint8_t>(best);
     }
-    idx[p] = static_cast<uint8_t>(best);
+  } else {
+    for (int p = threadIdx.x; p < ix.P; p += blockDim.x) {
+      const uint32_t* pr = ix.perms + static_cast<size_t>(p) * ix.K;
+      uint32_t best = 0;
+      float bv = h[__ldg(pr)];
+      for (int k = 1; k < ix.K; ++k) {
+        const float v = h[__ldg(pr + k)];
+        if (v > bv) {
+          bv = v;
+          best = k;
+        }
+      }
+      idx[p] = static_cast<uint8_t>(best);
+    }
   }
   __syncthreads();
   for (int w = threadIdx.x; w < ix.W; w += blockDim.x) {
@@ -114,45 +142,120 @@ __global__ void __launch_bounds__(512) k_probe_count(ProbeArgs a) {
   }
   __syncthreads();
   if (!count) return;
-  // K2: one warp per band; walk the span, count hits in the slice.
   uint32_t* bm = a.bitmap + static_cast<size_t>(s) * a.nwords;
   const uint32_t t = static_cast<uint32_t>(a.t);
-  for (int w = warp; w < ix.W; w += nwarp) {
-    uint32_t start, len;
-    if (!warp_probe(ix, w, codes[w], start, len)) continue;
-    const uint32_t* ids = ix.word_ids + static_cast<size_t>(w) * ix.V + start;
-    // 4 independent loads per lane in flight before the shared-memory updates
-    constexpr int U = 4;
-    for (uint32_t k0 = lane; k0 < len; k0 += 32 * U) {
-    uint32_t idu[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) idu[u] = k0 + 32 * u < len ? __ldg(ids + k0 + 32 * u) : 0xFFFFFFFFu;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t id = idu[u];
-      if (id < lo || id >= hi) continue;
-      const uint32_t local = id - lo;
-      if (bits) {
-        // level k holds "seen more than k times"; a visit climbs one level,
-        // the one after level t-2 marks the word (count == t)
-        const uint32_t wd = local >> 5, bit = 1u << (local & 31);
-        const uint32_t nw = a.slice_len >> 5;
-        int lvl = 0;
-        for (; lvl < a.levels; ++lvl)
-          if (!(atomicOr(cnt + lvl * nw + wd, bit) & bit)) break;
-        if (lvl == a.levels) atomicOr(cnt + a.levels * nw + wd, bit);
-        continue;
-      }
-      uint32_t c;
-      if (a.counter_bytes == 1) {
-        const uint32_t sh = (local & 3) * 8;
-        c = (atomicAdd(cnt + (local >> 2), 1u << sh) >> sh) & 0xFFu;
-      } else {
-        const uint32_t sh = (local & 1) * 16;
-        c = (atomicAdd(cnt + (local >> 1), 1u << sh) >> sh) & 0xFFFFu;
-      }
-      if (c + 1 == t) atomicOr(bm + (id >> 5), 1u << (id & 31));
+  auto count_id = [&](uint32_t id) {
+    if (id < lo || id >= hi) return;
+    const uint32_t local = id - lo;
+    if (bits) {
+      // level k holds "seen more than k times"; a visit climbs one level,
+      // the one after level t-2 marks the word (count == t)
+      const uint32_t wd = local >> 5, bit = 1u << (local & 31);
+      const uint32_t nw = a.slice_len >> 5;
+      int lvl = 0;
+      for (; lvl < a.levels; ++lvl)
+        if (!(atomicOr(cnt + lvl * nw + wd, bit) & bit)) break;
+      if (lvl == a.levels) atomicOr(cnt + a.levels * nw + wd, bit);
+      return;
     }
+    uint32_t c;
+    if (a.counter_bytes == 1) {
+      const uint32_t sh = (local & 3) * 8;
+      c = (atomicAdd(cnt + (local >> 2), 1u << sh) >> sh) & 0xFFu;
+    } else {
+      const uint32_t sh = (local & 1) * 16;
+      c = (atomicAdd(cnt + (local >> 1), 1u << sh) >> sh) & 0xFFFFu;
+    }
+    if (c + 1 == t) atomicOr(bm + (id >> 5), 1u << (id & 31));
+  };
+  constexpr int U = 4;  // id loads in flight per thread
+  if (ix.W <= kWarpBands) {
+    // K2, few bands (long spans): one warp per band, lanes 0/1 probe the two
+    // cuckoo tables, the span is walked coalesced.
+    for (int w = warp; w < ix.W; w += nwarp) {
+      uint32_t start, len;
+      if (!warp_probe(ix, w, codes[w], start, len)) continue;
+      const uint32_t* ids = ix.word_ids + static_cast<size_t>(w) * ix.V + start;
+      for (uint32_t k0 = lane; k0 < len; k0 += 32 * U) {
+        uint32_t idu[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) idu[u] = k0 + 32 * u < len ? __ldg(ids + k0 + 32 * u) : 0xFFFFFFFFu;
+#pragma unroll
+        for (int u = 0; u < U; ++u) count_id(idu[u]);
+      }
+    }
+  } else {
+    // K2, many bands (short spans) in three block-wide phases, so the
+    // dependent global round trips are paid once per row rather than once
+    // per band: (A) a thread per band probes both cuckoo tables; (B)
+    // exclusive scan of the span lengths; (C) the concatenated spans are
+    // walked flat, U id loads in flight per thread.
+    for (int w = threadIdx.x; w < ix.W; w += blockDim.x) {
+      const BandMeta m = ix.bands[w];
+      const uint32_t key = codes[w];
+      const uint32_t cap = 1u << m.lg;
+      const uint4 s0 = __ldg(ix.slots + m.slot_off + slot_of(m.mul0, m.lg, key));
+      const uint4 s1 = __ldg(ix.slots + m.slot_off + cap + slot_of(m.mul1, m.lg, key));
+      uint32_t st = 0, ln = 0;
+      if (s0.x == key) {  // table 0 wins (the reference probes it first)
+        st = s0.y;
+        ln = s0.z;
+      } else if (s1.x == key) {
+        st = s1.y;
+        ln = s1.z;
+      }
+      sp_start[w] = st;
+      sp_pre[w] = ln;
+    }
+    __syncthreads();
+    {  // exclusive scan of sp_pre[0..W) in place; sp_pre[W] = total
+      const int per = (ix.W + blockDim.x - 1) / blockDim.x;
+      const int b0 = min(ix.W, static_cast<int>(threadIdx.x) * per), b1 = min(ix.W, b0 + per);
+      uint32_t sum = 0;
+      for (int w = b0; w < b1; ++w) sum += sp_pre[w];
+      uint32_t x = sum;  // inclusive warp scan of the chunk sums
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      __shared__ uint32_t wsum[32];
+      if (lane == 31) wsum[warp] = x;
+      __syncthreads();
+      uint32_t off = 0, tot = 0;
+      for (int q = 0; q < nwarp; ++q) {
+        off += q < warp ? wsum[q] : 0u;
+        tot += wsum[q];
+      }
+      uint32_t run = off + x - sum;
+      for (int w = b0; w < b1; ++w) {
+        const uint32_t l = sp_pre[w];
+        sp_pre[w] = run;
+        run += l;
+      }
+      if (threadIdx.x == 0) sp_pre[ix.W] = tot;
+    }
+    __syncthreads();
+    const uint32_t total = sp_pre[ix.W];
+    for (uint32_t i0 = threadIdx.x; i0 < total; i0 += blockDim.x * U) {
+      uint32_t idu[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = i0 + blockDim.x * u;
+        idu[u] = 0xFFFFFFFFu;
+        if (i < total) {
+          int bl = 0, bh = ix.W - 1;  // band of flat position i: last w with sp_pre[w] <= i
+          while (bl < bh) {
+            const int mid = (bl + bh + 1) >> 1;
+            if (sp_pre[mid] <= i) bl = mid;
+            else bh = mid - 1;
+          }
+          idu[u] = __ldg(ix.word_ids + static_cast<size_t>(bl) * ix.V + sp_start[bl] +
+                         (i - sp_pre[bl]));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) count_id(idu[u]);
     }
   }
   if (bits) {  // OR this slice's marked words into the sentence bitmap
@@ -172,21 +275,29 @@ lsb_status launch_probe(lsb_ctx* ctx, const ProbeArgs& a) {
       a.t <= 0 ? 0
       : a.levels >= 0 ? static_cast<size_t>(a.levels + 1) * (a.slice_len / 8)
                       : ((static_cast<size_t>(a.slice_len) * a.counter_bytes + 15) & ~size_t(15));
-  const size_t smem = cbytes + ((ix.d + 3) & ~3) * 4 + ix.W * 4 + ix.P + 16;
+  const size_t smem = cbytes + ((ix.d + 3) & ~3) * 4 + (3 * ix.W + 1) * 4 + ix.P + 16;
   if (smem > ctx->smem_optin) {
     set_error("probe: shared memory budget exceeded");
     return LSB_EINVAL;
   }
-  static size_t configured = 0;
-  if (smem > configured) {
-    LSB_CUDA(cudaFuncSetAttribute(k_probe_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  dim3 grid0(a.S * a.B, std::max(1u, nslices));
+  const int threads = static_cast<int>(grid0.x * grid0.y) < ctx->sm_count ? 1024
+                      : a.levels >= 0                                       ? 256
+                                                                            : 512;
+  auto* kern = threads == 1024 ? k_probe_count<1024>
+               : threads == 512 ? k_probe_count<512>
+                                : k_probe_count<256>;
+  static size_t configured[3] = {0, 0, 0};
+  const int ki = threads == 1024 ? 2 : threads == 512 ? 1 : 0;
+  if (smem > configured[ki]) {
+    LSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
-    configured = smem;
+    configured[ki] = smem;
   }
-  dim3 grid(a.S * a.B, std::max(1u, nslices));
-  // bit-sliced counters need little shared memory: 256-thread CTAs, 8 per SM,
-  // so a 768-row step runs in one wave
-  LSB_CUDA(launch_pdl(ctx, k_probe_count, grid, dim3(a.levels >= 0 ? 256 : 512), smem, a));
+  // bit-sliced counters need little shared memory: 256-thread CTAs, 6 per SM,
+  // so a 768-row step runs in one wave; a grid smaller than the GPU gets
+  // 1024-thread CTAs (more loads in flight per row)
+  LSB_CUDA(launch_pdl(ctx, kern, grid0, dim3(threads), smem, a));
   LSB_LAUNCHED(ctx, "k_probe_count");
   return LSB_OK;
 }

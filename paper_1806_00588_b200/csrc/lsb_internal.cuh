@@ -155,25 +155,36 @@ __device__ __forceinline__ unsigned long long mix_seed_dev(unsigned long long se
 // Probe band w's two cuckoo slots for `key` with lanes 0 and 1 of the
 // calling warp in parallel (the lookup is <= 2 compares, band_index.cpp:73-83);
 // all lanes receive (found, start, len).
-__device__ __forceinline__ bool warp_probe(const IndexView& ix, int w, uint32_t key,
-                                           uint32_t& start, uint32_t& len) {
+// Cuckoo lookup of `key` in band w by a group of GS lanes (GS divides 32):
+// the group's lanes 0 / 1 probe tables 0 / 1, the hit is broadcast to the
+// group. Every lane of the warp must call it (warp-wide ballot / shuffles);
+// lanes of a group pass the same (w, key); `active` false = no probe.
+template <int GS>
+__device__ __forceinline__ bool group_probe(const IndexView& ix, int w, uint32_t key, bool active,
+                                            uint32_t& start, uint32_t& len) {
   const int lane = threadIdx.x & 31;
+  const int gl = lane & (GS - 1), gbase = lane & ~(GS - 1);
   bool hit = false;
   uint4 s = make_uint4(0, 0, 0, 0);
-  if (lane < 2) {
+  if (active && gl < 2) {
     const BandMeta m = ix.bands[w];
     const uint32_t cap = 1u << m.lg;
-    const uint32_t pos = m.slot_off + (lane ? cap + slot_of(m.mul1, m.lg, key)
-                                            : slot_of(m.mul0, m.lg, key));
+    const uint32_t pos = m.slot_off + (gl ? cap + slot_of(m.mul1, m.lg, key)
+                                          : slot_of(m.mul0, m.lg, key));
     s = __ldg(ix.slots + pos);
     hit = s.x == key;
   }
   const unsigned ballot = __ballot_sync(0xffffffffu, hit);
-  if (!ballot) return false;
-  const int src = __ffs(ballot) - 1;  // table 0 wins (it is probed first)
+  const unsigned mine = (ballot >> gbase) & 3u;
+  const int src = gbase + ((mine & 1u) ? 0 : 1);  // table 0 wins (it is probed first)
   start = __shfl_sync(0xffffffffu, s.y, src);
   len = __shfl_sync(0xffffffffu, s.z, src);
-  return true;
+  return mine != 0;
+}
+
+__device__ __forceinline__ bool warp_probe(const IndexView& ix, int w, uint32_t key,
+                                           uint32_t& start, uint32_t& len) {
+  return group_probe<32>(ix, w, key, true, start, len);
 }
 
 }  // namespace lsb

@@ -232,17 +232,20 @@ def test_softmax_examples(ctx):
         ctx.softmax_rows(np.full((1, 3), -np.inf, np.float32))
 
 
-@pytest.mark.parametrize("rows,n,B,nfz,ties", [
-    (12, 1335, 12, 0, False), (4, 50, 3, 2, False), (1, 4, 1, 0, False), (2, 3, 3, 0, False),
-    (5, 100, 12, 3, False), (50, 300, 50, 0, False), (30, 200, 40, 5, False),
-    (20, 64, 24, 2, True), (50, 50, 50, 0, True)])
-def test_expand_beams_parity(ctx, oracle, rows, n, B, nfz, ties):
+@pytest.mark.parametrize("rows,n,B,nfz,kind", [
+    (12, 1335, 12, 0, "rand"), (4, 50, 3, 2, "rand"), (1, 4, 1, 0, "rand"), (2, 3, 3, 0, "rand"),
+    (5, 100, 12, 3, "rand"), (50, 300, 50, 0, "rand"), (30, 200, 40, 5, "rand"),
+    (20, 64, 24, 2, "ties"), (50, 50, 50, 0, "ties"), (8, 1000, 12, 0, "ties"),
+    (6, 5000, 12, 0, "zeros"), (4, 3000, 40, 1, "zeros"), (3, 6000, 50, 0, "rand")])
+def test_expand_beams_parity(ctx, oracle, rows, n, B, nfz, kind):
     rng = np.random.default_rng(rows * 100 + n)
     logits = rng.standard_normal((rows, n)).astype(np.float32) * 2
-    if ties:  # equal scores everywhere: order decided by (beam, word) alone
+    if kind == "ties":  # equal scores everywhere: order decided by (beam, word) alone
         logits[:] = 0.0
+    elif kind == "zeros":  # peaked rows: most probabilities underflow to exactly 0
+        logits *= 150.0
     probs = oracle.softmax_rows(logits)
-    cum = np.zeros(rows) if ties else -rng.random(rows) * 3
+    cum = np.zeros(rows) if kind == "ties" else -rng.random(rows) * 3
     live = np.arange(nfz, nfz + rows, dtype=np.uint32)
     frozen = [(-rng.random() * 2, i) for i in range(nfz)]
     id_map = np.sort(rng.choice(10 * n, n, replace=False)).astype(np.uint32)

@@ -59,6 +59,8 @@ CASES = [
     # > 2048 candidates in registers, K5b head pruning (B > 16)
     (6000, 64, 8, 3, 16, 2, 50, 2200, 2),
     (4000, 64, 4, 2, 8, 2, 24, 100, 1),
+    # rows longer than the register path (n > 3072): global threshold path
+    (8000, 64, 8, 3, 16, 2, 12, 4000, 2),
 ]
 
 
