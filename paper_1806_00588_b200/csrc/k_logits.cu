@@ -392,7 +392,7 @@ static lsb_status launch_variant(lsb_ctx* ctx, const LogitsArgs& a, int grid) {
   return LSB_OK;
 }
 
-template <int RB, int CB, bool PARITY, int KC = 32, bool TWO_D = false>
+template <int RB, int CB, bool PARITY, int KC = 32, bool TWO_D = false, int NSO = 0>
 static lsb_status launch_logits_rb(lsb_ctx* ctx, LogitsArgs a, int target) {
   constexpr int CT = tile_cols<CB, TWO_D>();
   const int rgroups = (a.R_total + RB - 1) / RB;
@@ -410,6 +410,9 @@ static lsb_status launch_logits_rb(lsb_ctx* ctx, LogitsArgs a, int target) {
   if (grid == 0) return LSB_OK;
   const bool vec = (a.d & 3) == 0 && (reinterpret_cast<uintptr_t>(a.E) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(a.H) & 15) == 0;
+  if constexpr (NSO > 0)  // explicit ring depth (small batches: latency-bound)
+    return vec ? launch_variant<RB, CB, PARITY, true, NSO, KC, TWO_D>(ctx, a, grid)
+               : launch_variant<RB, CB, PARITY, false, NSO, KC, TWO_D>(ctx, a, grid);
   // Survivor-only launches (the shared block went to the tensor cores) have
   // no other CTAs to hide their L2 latency behind: 3-stage ring instead of 2.
   if (a.skip_shared)
@@ -453,14 +456,27 @@ lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_c
   // us; 1-D 6x2 with 16-float chunks 151 us; 4 CTAs/SM at 128 registers
   // 116 us; TMA bulk row copies 129 us (the per-lane operands serialise).
   static const bool one_d = getenv("LSB_K4_1D") != nullptr;
+  // Small batches (a few sentences) fill a fraction of the GPU and each CTA
+  // waits on its chunk loads: 32-column tiles (4x the CTAs) and an 8-deep ring.
+  // (Measured, cfg 2 shapes: S=1 36 -> 18 us, S=8 49 -> 29, S=16 66 -> 49,
+  // S=32 equal.) "Small" = the 128-column tiling would give at most two CTAs
+  // per SM; without a shared block assume ~10 survivor tiles per row group.
+  static const bool no_small = getenv("LSB_K4_NO_SMALL") != nullptr;
+  const int rb = choose_rb(a.Bsent);
+  const long est = static_cast<long>((a.R_total + rb - 1) / rb) *
+                   (a.n_shared ? static_cast<long>((a.n_shared + 127) / 128) : 10L);
+  const bool small = !no_small && est <= 2L * ctx->sm_count;
 #define LSB_RB2(R)                                                                   \
   case R:                                                                            \
+    if (!one_d && small)                                                             \
+      return fast ? launch_logits_rb<R, 1, false, 32, true, 8>(ctx, a, target_ctas)  \
+                  : launch_logits_rb<R, 1, true, 32, true, 8>(ctx, a, target_ctas);  \
     if (!one_d)                                                                      \
       return fast ? launch_logits_rb<R, 4, false, 32, true>(ctx, a, target_ctas)     \
                   : launch_logits_rb<R, 4, true, 32, true>(ctx, a, target_ctas);     \
     return fast ? launch_logits_rb<R, 1, false>(ctx, a, target_ctas)                 \
                 : launch_logits_rb<R, 1, true>(ctx, a, target_ctas);
-  switch (choose_rb(a.Bsent)) {
+  switch (rb) {
     LSB_RB2(16)
     LSB_RB2(12)
     LSB_RB(10)
