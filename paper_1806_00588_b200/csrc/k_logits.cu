@@ -109,6 +109,28 @@ __device__ __forceinline__ unsigned long long f2fma(unsigned long long a, unsign
   return d;
 }
 
+// FAST with paired FP32: each output keeps two partial FFMA chains (even /
+// odd d) in one f32x2 register pair, one FFMA2 per two MACs; summed in the
+// epilogue (FAST's tolerance, not the reference order).
+template <int RB, int CB, int KS>
+__device__ __forceinline__ void mac4_f2(unsigned long long (&acc)[RB][CB], const float* Es,
+                                        const float* Hs, int rbase, int cbase, int cstride,
+                                        int k4) {
+  ulonglong2 e[CB];
+#pragma unroll
+  for (int cb = 0; cb < CB; ++cb)
+    e[cb] = *reinterpret_cast<const ulonglong2*>(Es + (cbase + cb * cstride) * KS + k4 * 4);
+#pragma unroll
+  for (int rb = 0; rb < RB; ++rb) {
+    const ulonglong2 h = *reinterpret_cast<const ulonglong2*>(Hs + (rbase + rb) * KS + k4 * 4);
+#pragma unroll
+    for (int cb = 0; cb < CB; ++cb) {
+      acc[rb][cb] = f2fma(h.x, e[cb].x, acc[rb][cb]);
+      acc[rb][cb] = f2fma(h.y, e[cb].y, acc[rb][cb]);
+    }
+  }
+}
+
 template <int RB, int CB, int KS>
 __device__ __forceinline__ void mac4_x2(unsigned long long (&acc)[RB][CB][2], const float* Es,
                                         const float* Hs, int rbase, int cbase, int cstride, int k4,
@@ -246,13 +268,21 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
       for (int cb = 0; cb < TC; ++cb)
 #pragma unroll
         for (int k = 0; k < NA; ++k) acc[rb][cb][k] = 0.0f;
-    constexpr bool X2 = PARITY && VEC;  // paired FP32 path (see mac4_x2)
+    constexpr bool X2 = PARITY && VEC;   // paired FP32 path (see mac4_x2)
+    constexpr bool F2 = !PARITY && VEC;  // FAST paired path (see mac4_f2)
     unsigned long long acc2[X2 ? TR : 1][X2 ? TC : 1][2];
+    unsigned long long accf[F2 ? TR : 1][F2 ? TC : 1];
     if constexpr (X2) {
 #pragma unroll
       for (int rb = 0; rb < TR; ++rb)
 #pragma unroll
         for (int cb = 0; cb < TC; ++cb) acc2[rb][cb][0] = acc2[rb][cb][1] = 0ull;
+    }
+    if constexpr (F2) {
+#pragma unroll
+      for (int rb = 0; rb < TR; ++rb)
+#pragma unroll
+        for (int cb = 0; cb < TC; ++cb) accf[rb][cb] = 0ull;
     }
 
 #pragma unroll
@@ -285,6 +315,15 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
               mac4_x2<TR, TC, kKS>(acc2, Es, Hs, rbase, cbase, cstride, k4, a.x2_negzero,
                                    a.x2_one);
           }
+        } else if constexpr (F2) {
+          if (kv == kKC / 4) {
+#pragma unroll
+            for (int k4 = 0; k4 < kKC / 4; ++k4)
+              mac4_f2<TR, TC, kKS>(accf, Es, Hs, rbase, cbase, cstride, k4);
+          } else {
+            for (int k4 = 0; k4 < kv; ++k4)
+              mac4_f2<TR, TC, kKS>(accf, Es, Hs, rbase, cbase, cstride, k4);
+          }
         } else {
           if (kv == kKC / 4) {
 #pragma unroll
@@ -298,6 +337,14 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
       }
     }
     cp_async_wait<0>();
+    if constexpr (F2) {  // the two partial chains of each output
+#pragma unroll
+      for (int rb = 0; rb < TR; ++rb)
+#pragma unroll
+        for (int cb = 0; cb < TC; ++cb)
+          acc[rb][cb][0] = __uint_as_float(static_cast<uint32_t>(accf[rb][cb])) +
+                           __uint_as_float(static_cast<uint32_t>(accf[rb][cb] >> 32));
+    }
     if constexpr (X2) {  // unpack the pairs into the four reference lanes
 #pragma unroll
       for (int rb = 0; rb < TR; ++rb)
@@ -432,7 +479,12 @@ lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_c
   // contraction -> tcgen05 tensor cores; the per-sentence survivors stay on
   // the FFMA kernel below.
   static const bool tc_off = getenv("LSB_NO_TC") != nullptr;
-  if (fast && !tc_off && a.n_shared > 0 && a.R_total >= kTcMinRows && (a.d & 3) == 0 &&
+  // (The tensor-core block pays off for large dense blocks -- the full
+  // vocabulary; for a T = 1000 shared block the paired-FFMA tile was faster:
+  // 92 vs 97 us at cfg 2, before FAST used FFMA2.)
+  static const int tc_min_cols = getenv("LSB_TC_MIN_COLS") ? atoi(getenv("LSB_TC_MIN_COLS")) : 8192;
+  if (fast && !tc_off && a.n_shared >= static_cast<uint32_t>(std::max(1, tc_min_cols)) &&
+      a.R_total >= kTcMinRows && (a.d & 3) == 0 &&
       (reinterpret_cast<uintptr_t>(a.E) & 15) == 0 && (reinterpret_cast<uintptr_t>(a.H) & 15) == 0) {
     lsb_status rc;
     if (a.tc_A && a.tc_H) {
