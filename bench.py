@@ -245,9 +245,12 @@ def run_ours(args, rank, world, local):
                 "launches_timed": int(nrec),
                 "macs_per_launch": int(macs),
                 "fp32_tflops": round(flops / (logits_ms / 1e3) / 1e12, 2),
-                "note": "PARITY: FP32-issue bound (FMUL+FADD per MAC in the reference order); "
-                        "see fp32_issue" if mode == PARITY else
-                        "FAST: top-T block on tcgen05 (3xTF32), survivors on FFMA"}
+                "note": "PARITY: FMUL+FADD per MAC in the reference order as FFMA2 pairs; bound "
+                        "jointly by the FP32 pipe (fp32_issue) and shared-memory wavefronts "
+                        "(each 16-B LDS costs 4 wavefronts; ncu: ~60% of both)"
+                        if mode == PARITY else
+                        "FAST: paired FFMA2 chains (tcgen05 3xTF32 only for the full-vocabulary "
+                        "block)"}
     stages = {k: round(float(v) / max(nrec, 1), 5) for k, v in
               zip(["probe_count", "compact", "logits", "softmax_topb", "expand"], stage_tot)}
 
