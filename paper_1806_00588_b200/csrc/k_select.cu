@@ -488,10 +488,10 @@ __device__ void reorder_hidden(const ExpandArgs& a, int s, int count, const uint
 // Rank selection. Lists: [0, nfz) explicit frozen singletons, then one list
 // per hypothesis row (a finished row is a singleton carrying its score).
 // Shared memory: per list off/len (ints), then per candidate score, beam, word.
-constexpr int kExpT = 512;
 constexpr int kRankMaxLists = 128;
 
-__global__ void __launch_bounds__(kExpT) k_expand(ExpandArgs a) {
+template <int NT>
+__global__ void __launch_bounds__(NT) k_expand(ExpandArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_off[kRankMaxLists + 1];
   __shared__ uint32_t s_beams[64];
@@ -1067,13 +1067,17 @@ lsb_status launch_expand(lsb_ctx* ctx, const ExpandArgs& a) {
   const int nl = (a.frozen_mode ? a.nfrozen : 0) + a.Bsent;
   const size_t rank_smem = static_cast<size_t>(nl) * std::max(a.topB, 1) * (8 + 8 + 4 + 4 + 4 + 4);
   if (nl <= kRankMaxLists && rank_smem <= ctx->smem_optin) {
-    static size_t configured = 0;
-    if (rank_smem > configured) {
-      LSB_CUDA(cudaFuncSetAttribute(k_expand, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    // 1024 threads for small beams (cfg 2: 132.5 -> 131.3 us/step), 512 for
+    // large ones (cfg 3, B=50: 49 vs 61 us)
+    const bool wide = a.topB <= 16;
+    auto* kern = wide ? k_expand<1024> : k_expand<512>;
+    static size_t configured[2] = {0, 0};
+    if (rank_smem > configured[wide]) {
+      LSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(rank_smem)));
-      configured = rank_smem;
+      configured[wide] = rank_smem;
     }
-    LSB_CUDA(launch_pdl(ctx, k_expand, dim3(a.S), dim3(kExpT), rank_smem, a));
+    LSB_CUDA(launch_pdl(ctx, kern, dim3(a.S), dim3(wide ? 1024 : 512), rank_smem, a));
     LSB_LAUNCHED(ctx, "k_expand");
     return LSB_OK;
   }
