@@ -390,19 +390,20 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     }
   }
   __syncthreads();
-  // [0, T) prefix, then per-thread contiguous word ranges for the ordered emit
+  // Every id < T is a candidate (the top-T merge), so positions [0, T) hold
+  // 0..T-1 -- written coalesced by all threads -- and an id >= T sits at
+  // T + its rank among the set bits >= T: per-thread contiguous word ranges,
+  // one block scan, ordered emit of the (few) bits above the prefix.
+  for (uint32_t i = threadIdx.x; i < a.T; i += blockDim.x) ids[i] = i;
   const uint32_t per = (nw + blockDim.x - 1) / blockDim.x;
   const uint32_t w0 = threadIdx.x * per, w1 = min(nw, w0 + per);
   uint32_t cnt = 0;
-  for (uint32_t w = w0; w < w1; ++w) {
-    const uint32_t m = bm[w] | below_mask(w, a.T);
-    bm[w] = m;
-    cnt += __popc(m);
-  }
+  for (uint32_t w = w0; w < w1; ++w) cnt += __popc(bm[w] & ~below_mask(w, a.T));
   uint32_t total;
-  uint32_t base = block_scan_excl(cnt, wsum, &total);
+  uint32_t base = a.T + block_scan_excl(cnt, wsum, &total);
+  total += a.T;
   for (uint32_t w = w0; w < w1; ++w) {
-    uint32_t m = bm[w];
+    uint32_t m = bm[w] & ~below_mask(w, a.T);
     while (m) {
       const int b = __ffs(m) - 1;
       ids[base++] = w * 32 + b;
