@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(kLT, MINB ? MINB : (kStages == 2 ? 5 : 3)) k_l
           acc[rb][cb][3] = __uint_as_float(static_cast<uint32_t>(acc2[rb][cb][1] >> 32));
         }
     }
+    pdl_trigger();
     // the d mod 4 tail (all of d when d < 4) sits in the last chunk: lane 0
     if (d4 < d && warp_live) {
       const int cl = (nchunks - 1) * kKC;

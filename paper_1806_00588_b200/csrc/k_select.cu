@@ -178,6 +178,7 @@ __device__ __forceinline__ void row_registers(const SoftmaxArgs& a, int row, flo
         }
       }
     __syncthreads();
+    pdl_trigger();
     const int nc = s_nc;
     const int keep = static_cast<int>(min(static_cast<uint32_t>(B), n));
     if (nc <= kSelCand) {
@@ -651,6 +652,7 @@ __global__ void __launch_bounds__(NT) k_expand(ExpandArgs a) {
     s_count = count;
   }
   __syncthreads();
+  pdl_trigger();
   if (a.hidden_out && a.hidden) reorder_hidden(a, s, min(s_count, 64), s_beams);
 }
 

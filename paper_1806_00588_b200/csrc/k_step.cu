@@ -29,9 +29,6 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(
   const IndexView& ix = a.ix;
   const int row = blockIdx.x;
   const int s = row / a.B, i = row % a.B;
-  pdl_wait();
-  if (a.n_hyp && i >= a.n_hyp[s]) return;
-  if (a.finished && a.finished[row]) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const uint32_t lo = blockIdx.y * a.slice_len;
   const uint32_t hi = min(ix.V, lo + a.slice_len);
@@ -49,6 +46,9 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(
   uint32_t* sp_pre = sp_start + ix.W;   // ... and exclusive prefix of span lengths [W + 1]
   uint8_t* idx = reinterpret_cast<uint8_t*>(sp_pre + ix.W + 1);
 
+  __shared__ BandMeta s_bands[kWarpBands];  // few-band path: probe metadata
+  if (ix.W <= kWarpBands)
+    for (int w = threadIdx.x; w < ix.W; w += blockDim.x) s_bands[w] = ix.bands[w];
   for (size_t k = threadIdx.x; k < cbytes / 16; k += blockDim.x)
     reinterpret_cast<uint4*>(cnt)[k] = make_uint4(0, 0, 0, 0);
   // this thread's permutation row, fetched while the hidden row is in flight
@@ -60,6 +60,10 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(
 #pragma unroll
     for (int k = 0; k < kMaxKReg; ++k) pk[k] = k < ix.K ? __ldg(pr + k) : 0u;
   }
+  // everything above reads only the index (static); the step inputs below
+  // may come from the previous kernel
+  pdl_wait();
+  const bool dead = (a.n_hyp && i >= a.n_hyp[s]) || (a.finished && a.finished[row]);
   const float* src = a.hidden + static_cast<size_t>(row) * ix.d;
   int nan = 0;
   if ((ix.d & 3) == 0) {
@@ -75,6 +79,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(
       h[c] = v;
     }
   }
+  if (dead) return;  // uniform per CTA
   if (__syncthreads_or(nan)) {
     if (threadIdx.x == 0) atomicOr(a.err, kErrNaN);
     return;
@@ -170,11 +175,31 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(
   };
   constexpr int U = 4;  // id loads in flight per thread
   if (ix.W <= kWarpBands) {
-    // K2, few bands (long spans): one warp per band, lanes 0/1 probe the two
-    // cuckoo tables, the span is walked coalesced.
-    for (int w = warp; w < ix.W; w += nwarp) {
-      uint32_t start, len;
-      if (!warp_probe(ix, w, codes[w], start, len)) continue;
+    // K2, few bands (long spans): one warp per band. A warp's bands (at most
+    // 16) are probed in one round trip -- lanes 2j / 2j+1 probe tables 0 / 1
+    // of band j, metadata from shared memory -- then each span is walked
+    // coalesced, U loads in flight per lane.
+    const int nb = warp < ix.W ? (ix.W - warp + nwarp - 1) / nwarp : 0;
+    const int j = lane >> 1;
+    uint4 sl = make_uint4(0, 0, 0, 0);
+    bool hit = false;
+    if (j < nb) {
+      const int w = warp + j * nwarp;
+      const BandMeta m = s_bands[w];
+      const uint32_t key = codes[w];
+      const uint32_t pos = m.slot_off + ((lane & 1) ? (1u << m.lg) + slot_of(m.mul1, m.lg, key)
+                                                    : slot_of(m.mul0, m.lg, key));
+      sl = __ldg(ix.slots + pos);
+      hit = sl.x == key;
+    }
+    const unsigned ballot = __ballot_sync(0xffffffffu, hit);
+    for (int jj = 0; jj < nb; ++jj) {
+      const unsigned two = (ballot >> (2 * jj)) & 3u;
+      if (!two) continue;
+      const int src = 2 * jj + ((two & 1u) ? 0 : 1);  // table 0 wins (probed first)
+      const uint32_t start = __shfl_sync(0xffffffffu, sl.y, src);
+      const uint32_t len = __shfl_sync(0xffffffffu, sl.z, src);
+      const int w = warp + jj * nwarp;
       const uint32_t* ids = ix.word_ids + static_cast<size_t>(w) * ix.V + start;
       for (uint32_t k0 = lane; k0 < len; k0 += 32 * U) {
         uint32_t idu[U];
@@ -258,6 +283,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(
       for (int u = 0; u < U; ++u) count_id(idu[u]);
     }
   }
+  pdl_trigger();
   if (bits) {  // OR this slice's marked words into the sentence bitmap
     __syncthreads();
     const uint32_t nw = a.slice_len >> 5;
@@ -394,6 +420,7 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
   // 0..T-1 -- written coalesced by all threads -- and an id >= T sits at
   // T + its rank among the set bits >= T: per-thread contiguous word ranges,
   // one block scan, ordered emit of the (few) bits above the prefix.
+  pdl_trigger();
   for (uint32_t i = threadIdx.x; i < a.T; i += blockDim.x) ids[i] = i;
   const uint32_t per = (nw + blockDim.x - 1) / blockDim.x;
   const uint32_t w0 = threadIdx.x * per, w1 = min(nw, w0 + per);

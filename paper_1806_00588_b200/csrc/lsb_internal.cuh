@@ -115,6 +115,12 @@ namespace lsb {
 // predecessor's results are visible and must precede every read of them.
 // Without the launch attribute it returns immediately.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// Lets the next kernel on the stream launch once every CTA of this grid has
+// called it (or exited); that kernel still waits for this grid's completion
+// in pdl_wait(), so placement only affects overlap, never correctness.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(lsb_ctx* ctx, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
