@@ -67,5 +67,6 @@ def test_reference_acceptance_criteria_1_to_8():
     cli = CLI if os.path.exists(CLI) else "/nonexistent/lshbeam_cli"
     r = subprocess.run([exe, cli], capture_output=True, text=True, timeout=1500, cwd=BUILD)
     status = dict(re.findall(r"criterion (\d+): (PASS|FAIL)", r.stdout))
+    print("\n".join(l for l in r.stdout.splitlines() if l.startswith("criterion")))
     for c in map(str, range(1, 10 if os.path.exists(CLI) else 9)):
         assert status.get(c) == "PASS", r.stdout[-3000:]
