@@ -79,6 +79,10 @@ lsb_status lsb_ctx_destroy(lsb_ctx* c) {
   if (!c) return LSB_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->side) cudaStreamSynchronize(c->side);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->fork) cudaEventDestroy(c->fork);
+  if (c->join) cudaEventDestroy(c->join);
   if (c->err_dev) cudaFree(c->err_dev);
   if (c->err_host) cudaFreeHost(c->err_host);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

@@ -473,6 +473,9 @@ static lsb_status launch_logits_rb(lsb_ctx* ctx, LogitsArgs a, int target) {
              : launch_variant<RB, CB, PARITY, false, 2, KC, TWO_D>(ctx, a, grid);
 }
 
+static lsb_status launch_logits_survivors(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode,
+                                          int target_ctas);
+
 // One column per thread, RB rows: 8 FP instructions (PARITY) or 4 FFMA
 // (FAST) per 16-byte E load; 5 CTAs per SM.
 lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_ctas) {
@@ -486,10 +489,24 @@ lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_c
   // (The tensor-core block pays off for large dense blocks -- the full
   // vocabulary; for a T = 1000 shared block the paired-FFMA tile was faster:
   // 92 vs 97 us at cfg 2, before FAST used FFMA2.)
-  static const int tc_min_cols = getenv("LSB_TC_MIN_COLS") ? atoi(getenv("LSB_TC_MIN_COLS")) : 8192;
+  static const int tc_min_cols = getenv("LSB_TC_MIN_COLS") ? atoi(getenv("LSB_TC_MIN_COLS")) : 1;
   if (fast && !tc_off && a.n_shared >= static_cast<uint32_t>(std::max(1, tc_min_cols)) &&
-      a.R_total >= kTcMinRows && (a.d & 3) == 0 &&
+      a.R_total >= (a.ids ? 4 * kTcMinRows : kTcMinRows) && (a.d & 3) == 0 &&
       (reinterpret_cast<uintptr_t>(a.E) & 15) == 0 && (reinterpret_cast<uintptr_t>(a.H) & 15) == 0) {
+    // With survivors to score, the tensor-core block goes to a side stream
+    // (fork / join events) so it overlaps the survivor tiles on this one.
+    const bool overlap = a.ids && a.S > 0;
+    cudaStream_t main_stream = ctx->stream;
+    if (overlap) {
+      if (!ctx->side) {
+        LSB_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        LSB_CUDA(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming));
+        LSB_CUDA(cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming));
+      }
+      LSB_CUDA(cudaEventRecord(ctx->fork, main_stream));
+      LSB_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));
+      ctx->stream = ctx->side;
+    }
     lsb_status rc;
     if (a.tc_A && a.tc_H) {
       rc = launch_tf32_tile(ctx, a.H, a.R_total, a.d, a.tc_N, a.tc_H);
@@ -499,10 +516,22 @@ lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_c
     } else {
       rc = launch_tc_logits(ctx, a.H, a.R_total, a.E, a.bias, a.d, 0, a.n_shared, a.out, a.ldo, 0);
     }
+    ctx->stream = main_stream;
     if (rc) return rc;
     a.skip_shared = 1;
-    if (!a.ids || a.S == 0) return LSB_OK;
+    if (!overlap) return LSB_OK;
+    LSB_CUDA(cudaEventRecord(ctx->join, ctx->side));
+    lsb_status rs = launch_logits_survivors(ctx, a, mode, target_ctas);
+    LSB_CUDA(cudaStreamWaitEvent(main_stream, ctx->join, 0));
+    return rs;
   }
+  return launch_logits_survivors(ctx, a, mode, target_ctas);
+}
+
+// The FFMA tiles: the whole candidate set, or (skip_shared) the survivors.
+static lsb_status launch_logits_survivors(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode,
+                                          int target_ctas) {
+  const bool fast = mode == LSB_MODE_FAST;
 #define LSB_RB(R)                                                        \
   case R:                                                                \
     return fast ? launch_logits_rb<R, 1, false>(ctx, a, target_ctas)     \
@@ -523,7 +552,11 @@ lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_c
   const int rb = choose_rb(a.Bsent);
   const long est = static_cast<long>((a.R_total + rb - 1) / rb) *
                    (a.n_shared ? static_cast<long>((a.n_shared + 127) / 128) : 10L);
-  const bool small = !no_small && est <= 2L * ctx->sm_count;
+  // survivor-only launches (the shared block went to the tensor cores):
+  // assume ~3 column tiles of 128 per row group
+  const long est_surv = static_cast<long>(a.S) * ((a.Bsent + rb - 1) / rb) * 3L;
+  const bool small = !no_small && (a.skip_shared ? est_surv <= 2L * ctx->sm_count
+                                                 : est <= 2L * ctx->sm_count);
 #define LSB_RB2(R)                                                                   \
   case R:                                                                            \
     if (!one_d && small)                                                             \

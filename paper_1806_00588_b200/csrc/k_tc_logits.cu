@@ -310,6 +310,8 @@ static lsb_status launch_tc_n(lsb_ctx* ctx, const TcLogitsArgs& a) {
 
 // Widest tile that still gives every SM work (narrower tiles re-read E more).
 int tc_rows_per_tile(lsb_ctx* ctx, int rows, uint32_t ncols) {
+  static const int force = getenv("LSB_TC_N") ? atoi(getenv("LSB_TC_N")) : 0;
+  if (force == 64 || force == 128) return force;
   const long long mt = (ncols + tc::kM - 1) / tc::kM;
   if (mt * ((rows + 127) / 128) >= 2 * ctx->sm_count) return 128;
   return 64;  // N = 32 measured slower: TMA latency exposed with 2 stages

@@ -61,6 +61,10 @@ struct lsb_ctx {
   uint64_t launches = 0;
   int cuckoo_parallel = 0;        // 0: reference slot placement
   int pdl = 1;                    // programmatic dependent launch between step kernels
+  // FAST: the tensor-core shared block runs on a side stream concurrently
+  // with the survivor tiles (created on first use)
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 struct lsb_model {
