@@ -33,12 +33,14 @@ __device__ __forceinline__ bool top_better(float pa, uint32_t ra, float pb, uint
   return pa > pb || (pa == pb && ra < rb);
 }
 
-template <class T, class Op>
+// Block-wide reduction through red[kSelT / 32]. FIRST: red is used for the
+// first time in this CTA, so no barrier is needed before overwriting it.
+template <class T, class Op, bool FIRST = false>
 __device__ __forceinline__ T block_reduce(T v, T* red, Op op) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
-  __syncthreads();  // red[] may still be read from a previous reduction
+  if constexpr (!FIRST) __syncthreads();  // red[] may still be read from a previous reduction
   if (lane == 0) red[warp] = v;
   __syncthreads();
   v = red[0];
@@ -47,11 +49,21 @@ __device__ __forceinline__ T block_reduce(T v, T* red, Op op) {
   return v;
 }
 
+struct FMaxOp {
+  __device__ float operator()(float x, float y) const { return (x < y) ? y : x; }
+};
+struct DSumOp {
+  __device__ double operator()(double x, double y) const { return x + y; }
+};
+__device__ constexpr FMaxOp fmax_op{};
+__device__ constexpr DSumOp dsum_op{};
+
 // The K-th largest of the CTA's kSelT per-thread values x (-1 = none): each
 // warp sorts its 32 with a shuffle bitonic network, every lane ranks its value
 // against the other warps' sorted lists in (value desc, position asc) order.
 // K lanes hold an entry >= the result, so it bounds the row's K-th largest
-// from below. Returns -1 when K > kSelT. Contains barriers (whole CTA).
+// from below. Returns -1 when K > kSelT. Contains barriers (whole CTA); call
+// it at most once per CTA (its shared scratch is not protected for reuse).
 __device__ __forceinline__ float kth_lane_max(float x, int K) {
   __shared__ float s_lm[kSelT];
   __shared__ float s_tau;
@@ -73,7 +85,6 @@ __device__ __forceinline__ float kth_lane_max(float x, int K) {
     float t = s_lm[0];
 #pragma unroll
     for (int w = 1; w < kSelT / 32; ++w) t = fmaxf(t, s_lm[w]);
-    __syncthreads();  // s_lm may be reused by the next call
     return t;
   }
   s_lm[tid] = x;
@@ -97,9 +108,7 @@ __device__ __forceinline__ float kth_lane_max(float x, int K) {
     if (rank == K - 1) s_tau = x;
   }
   __syncthreads();
-  const float t = s_tau;
-  __syncthreads();  // s_lm / s_tau may be reused by the next call
-  return t;
+  return s_tau;
 }
 
 // Rows of at most kSelT * kSelReg candidates (the LSH step's): the row lives
@@ -125,7 +134,7 @@ __device__ __forceinline__ void row_registers(const SoftmaxArgs& a, int row, flo
     v[k] = c < n ? L[c] : -INFINITY;
     mx = (mx < v[k]) ? v[k] : mx;
   }
-  mx = block_reduce(mx, red_f, [](float x, float y) { return (x < y) ? y : x; });
+  mx = block_reduce<float, decltype(fmax_op), true>(mx, red_f, fmax_op);
   if (n == 0 || (isinf(mx) && mx < 0)) {
     if (tid == 0) {
       atomicOr(a.err, kErrEmptyRow);
@@ -143,7 +152,7 @@ __device__ __forceinline__ void row_registers(const SoftmaxArgs& a, int row, flo
       sum += e;
     }
   }
-  sum = block_reduce(sum, red_d, [](double x, double y) { return x + y; });
+  sum = block_reduce<double, decltype(dsum_op), true>(sum, red_d, dsum_op);
   const float inv = static_cast<float>(1.0 / sum);
 #pragma unroll
   for (int k = 0; k < REG; ++k) {
@@ -278,7 +287,7 @@ __global__ void __launch_bounds__(kSelT) k_softmax_topb(SoftmaxArgs a) {
       const float v = L[r];
       mx = (mx < v) ? v : mx;
     }
-    mx = block_reduce(mx, red_f, [](float x, float y) { return (x < y) ? y : x; });
+    mx = block_reduce<float, decltype(fmax_op), true>(mx, red_f, fmax_op);
     if (n == 0 || (isinf(mx) && mx < 0)) {
       if (tid == 0) {
         atomicOr(a.err, kErrEmptyRow);
@@ -293,7 +302,7 @@ __global__ void __launch_bounds__(kSelT) k_softmax_topb(SoftmaxArgs a) {
       L[r] = static_cast<float>(e);
       sum += e;
     }
-    sum = block_reduce(sum, red_d, [](double x, double y) { return x + y; });
+    sum = block_reduce<double, decltype(dsum_op), true>(sum, red_d, dsum_op);
     inv = static_cast<float>(1.0 / sum);
   }
   if (B <= 0) {
