@@ -442,6 +442,9 @@ static lsb_status launch_variant(lsb_ctx* ctx, const LogitsArgs& a, int grid) {
   return LSB_OK;
 }
 
+static const int kMinSurvivorCtas =
+    getenv("LSB_K4_MIN_SURV") ? atoi(getenv("LSB_K4_MIN_SURV")) : 4;
+
 template <int RB, int CB, bool PARITY, int KC = 32, bool TWO_D = false, int NSO = 0,
           int MINB = 0>
 static lsb_status launch_logits_rb(lsb_ctx* ctx, LogitsArgs a, int target) {
@@ -452,7 +455,9 @@ static lsb_status launch_logits_rb(lsb_ctx* ctx, LogitsArgs a, int target) {
   a.G = (a.Bsent + RB - 1) / RB;
   if (a.ids && a.S > 0) {
     const size_t max_tiles = (a.ncap > a.n_shared ? a.ncap - a.n_shared : 0) / CT + 1;
-    const int want = std::max(1, (target - a.jobs_shared) / std::max(1, a.S * a.G));
+    // at least 4 CTAs per row group: a large shared block must not leave each
+    // sentence's ~3 survivor tiles to one CTA in series (S=128: 283 -> see DESIGN)
+    const int want = std::max(kMinSurvivorCtas, (target - a.jobs_shared) / std::max(1, a.S * a.G));
     a.X = static_cast<int>(std::min<size_t>({static_cast<size_t>(want), size_t(64), max_tiles}));
   } else {
     a.X = 0;
