@@ -194,3 +194,45 @@ def test_step_host_async_matches_sync(ctx, oracle):
         got = [[(ch[s * B + j].score, ch[s * B + j].beam, ch[s * B + j].word)
                 for j in range(int(nc[s]))] for s in range(S)]
         assert got == want[k]
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_step_fuzz(ctx, oracle, seed):
+    """Random shapes across every kernel variant the step picks: many bands
+    (W > 64: the phased probe), large beams (threshold top-B for B > 32, K5b
+    head pruning for B > 16), rows longer than the register path, odd d,
+    small and larger batches (32-column K4 tiles or 128-column ones), frozen
+    and short hypotheses. Everything compared exactly (PARITY)."""
+    rng = np.random.default_rng(1000 + seed)
+    V = int(rng.integers(300, 6000))
+    d = int(rng.choice([16, 33, 64, 67, 128]))
+    K = int(rng.choice([2, 4, 8, 16]))
+    u = int(rng.integers(1, 4))
+    W = int(rng.choice([4, 16, 40, 80, 200]))
+    S = int(rng.choice([1, 3, 9, 24]))
+    B = int(rng.choice([1, 3, 12, 20, 40]))
+    T = int(rng.choice([0, 10, V // 3, V // 2, V]))
+    t = int(rng.integers(1, 5))
+    frozen = bool(rng.integers(0, 2)) and B > 2
+    E, bias, perms, bt, ps, isd = make_world(oracle, V, d, K, u, W, seed=seed + 17,
+                                             bias_strength=float(rng.choice([0.0, 8.0])))
+    specials = sorted({V - 1, int(rng.integers(0, V))})
+    state = make_state(oracle, S, B, d, seed=seed * 7 + 1, frozen_every=3 if frozen else 0,
+                       short=(B // 2 if frozen else 0))
+    b, res, hout = run_gpu(ctx, E, bias, V, d, K, u, W, ps, isd, S, B, T, t, specials, state)
+    hidden, scores, finished, n_hyp = state
+    for s in range(S):
+        want = oracle_step(oracle, bt, perms, E, bias, K, u, W, hidden[s], scores[s],
+                           finished[s], int(n_hyp[s]), B, T, t, specials)
+        ids, prov = b.candidates(s)
+        np.testing.assert_array_equal(ids, want["ids"])
+        assert prov == want["prov"]
+        probs = b.probs(s)
+        np.testing.assert_array_equal(probs.view(np.uint32), want["probs"].view(np.uint32))
+        ws, wb, ww = want["choices"]
+        assert len(res[s]) == len(ws)
+        np.testing.assert_array_equal(np.array([c[2] for c in res[s]]), ww)
+        np.testing.assert_array_equal(np.array([c[1] for c in res[s]]), wb)
+        np.testing.assert_array_equal(np.array([c[0] for c in res[s]]), ws)
+        for k, (_, beam, _) in enumerate(res[s]):
+            np.testing.assert_array_equal(hout[s, k], hidden[s, beam])
