@@ -236,3 +236,34 @@ def test_step_fuzz(ctx, oracle, seed):
         np.testing.assert_array_equal(np.array([c[0] for c in res[s]]), ws)
         for k, (_, beam, _) in enumerate(res[s]):
             np.testing.assert_array_equal(hout[s, k], hidden[s, beam])
+
+
+@pytest.mark.parametrize("full", [False, True])
+def test_fast_step_tensor_cores(ctx, oracle, full):
+    """FAST with enough rows for the tcgen05 block: the top-T shared block on
+    the side stream beside the survivor FFMA tiles (LSH, >= 256 rows), or the
+    whole vocabulary (full, >= 64 rows). Candidates are exact; probabilities
+    and scores within FAST's tolerance; choices agree except at near-ties."""
+    V, d, K, u, W = 4000, 64, 8, 3, 16
+    S, B, T, t = (32, 12, 1000, 2) if not full else (12, 6, 0, 0)
+    E, bias, perms, bt, ps, isd = make_world(oracle, V, d, K, u, W, seed=23, bias_strength=8.0)
+    state = make_state(oracle, S, B, d, seed=29)
+    b, res, _ = run_gpu(ctx, E, bias, V, d, K, u, W, ps, isd, S, B, T, t, [V - 1], state,
+                        mode=1, full=full)
+    hidden, scores, finished, n_hyp = state
+    agree = total = 0
+    for s in range(S):
+        if full:
+            want = oracle_full_step(oracle, E, bias, hidden[s], scores[s], finished[s], B, B)
+        else:
+            want = oracle_step(oracle, bt, perms, E, bias, K, u, W, hidden[s], scores[s],
+                               finished[s], int(n_hyp[s]), B, T, t, [V - 1])
+            ids, prov = b.candidates(s)
+            np.testing.assert_array_equal(ids, want["ids"])
+            np.testing.assert_allclose(b.probs(s), want["probs"], rtol=2e-3, atol=1e-6)
+        ws, wb, ww = want["choices"]
+        got = [(c[1], c[2]) for c in res[s]]
+        agree += sum(g == (int(x), int(y)) for g, x, y in zip(got, wb, ww))
+        total += len(ws)
+        np.testing.assert_allclose(np.array([c[0] for c in res[s]]), ws, rtol=0, atol=1e-3)
+    assert agree >= 0.99 * total, (agree, total)
