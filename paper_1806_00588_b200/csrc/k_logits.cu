@@ -558,12 +558,17 @@ static lsb_status launch_logits_survivors(lsb_ctx* ctx, LogitsArgs a, lsb_mode m
   const long est = static_cast<long>((a.R_total + rb - 1) / rb) *
                    (a.n_shared ? static_cast<long>((a.n_shared + 127) / 128) : 10L);
   // survivor-only launches (the shared block went to the tensor cores):
-  // assume ~3 column tiles of 128 per row group
+  // assume ~3 column tiles of 128 per row group; small ones use 64-column
+  // tiles and a 4-deep ring (FAST cfg 2: 96.5 -> 89.2 us/step vs 32-column,
+  // 8-deep; 128-column 93.8)
   const long est_surv = static_cast<long>(a.S) * ((a.Bsent + rb - 1) / rb) * 3L;
   const bool small = !no_small && (a.skip_shared ? est_surv <= 2L * ctx->sm_count
                                                  : est <= 2L * ctx->sm_count);
 #define LSB_RB2(R)                                                                   \
   case R:                                                                            \
+    if (!one_d && small && a.skip_shared) /* survivors beside the TC block: */       \
+      return fast ? launch_logits_rb<R, 2, false, 32, true, 4>(ctx, a, target_ctas)  \
+                  : launch_logits_rb<R, 2, true, 32, true, 4>(ctx, a, target_ctas);  \
     if (!one_d && small)                                                             \
       return fast ? launch_logits_rb<R, 1, false, 32, true, 8>(ctx, a, target_ctas)  \
                   : launch_logits_rb<R, 1, true, 32, true, 8>(ctx, a, target_ctas);  \
