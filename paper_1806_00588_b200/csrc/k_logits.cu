@@ -155,9 +155,8 @@ __device__ __forceinline__ void mac4_x2(unsigned long long (&acc)[RB][CB][2], co
 // lanes of a row group and its E loads by the 4 of a column group, so one
 // 16-byte LDS is a single wavefront (vs 4 for 32 distinct E rows) and a
 // thread issues RB/4 + TC loads per 4-step instead of RB + 1.
-template <int RB, int CB, bool PARITY, bool VEC, int kStages, int KC, bool TWO_D = false,
-          int MINB = 0>
-__global__ void __launch_bounds__(kLT, MINB ? MINB : (kStages == 2 ? 5 : 3)) k_logits(LogitsArgs a) {
+template <int RB, int CB, bool PARITY, bool VEC, int kStages, int KC, bool TWO_D = false>
+__global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs a) {
   constexpr int kKC = KC;
   constexpr int kKS = KC + 4;
   constexpr int kParts = KC / 4;           // 16-byte pieces per row chunk
@@ -426,12 +425,11 @@ int choose_rb(int B) {
   return best;
 }
 
-template <int RB, int CB, bool PARITY, bool VEC, int NS, int KC = 32, bool TWO_D = false,
-          int MINB = 0>
+template <int RB, int CB, bool PARITY, bool VEC, int NS, int KC = 32, bool TWO_D = false>
 static lsb_status launch_variant(lsb_ctx* ctx, const LogitsArgs& a, int grid) {
   constexpr size_t smem = logits_smem_bytes<RB, CB, NS, KC, TWO_D>();
   static bool configured = false;
-  auto* kern = k_logits<RB, CB, PARITY, VEC, NS, KC, TWO_D, MINB>;
+  auto* kern = k_logits<RB, CB, PARITY, VEC, NS, KC, TWO_D>;
   if (!configured) {
     LSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
@@ -445,8 +443,7 @@ static lsb_status launch_variant(lsb_ctx* ctx, const LogitsArgs& a, int grid) {
 static const int kMinSurvivorCtas =
     getenv("LSB_K4_MIN_SURV") ? atoi(getenv("LSB_K4_MIN_SURV")) : 4;
 
-template <int RB, int CB, bool PARITY, int KC = 32, bool TWO_D = false, int NSO = 0,
-          int MINB = 0>
+template <int RB, int CB, bool PARITY, int KC = 32, bool TWO_D = false, int NSO = 0>
 static lsb_status launch_logits_rb(lsb_ctx* ctx, LogitsArgs a, int target) {
   constexpr int CT = tile_cols<CB, TWO_D>();
   const int rgroups = (a.R_total + RB - 1) / RB;
@@ -467,8 +464,8 @@ static lsb_status launch_logits_rb(lsb_ctx* ctx, LogitsArgs a, int target) {
   const bool vec = (a.d & 3) == 0 && (reinterpret_cast<uintptr_t>(a.E) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(a.H) & 15) == 0;
   if constexpr (NSO > 0)  // explicit ring depth (small batches: latency-bound)
-    return vec ? launch_variant<RB, CB, PARITY, true, NSO, KC, TWO_D, MINB>(ctx, a, grid)
-               : launch_variant<RB, CB, PARITY, false, NSO, KC, TWO_D, MINB>(ctx, a, grid);
+    return vec ? launch_variant<RB, CB, PARITY, true, NSO, KC, TWO_D>(ctx, a, grid)
+               : launch_variant<RB, CB, PARITY, false, NSO, KC, TWO_D>(ctx, a, grid);
   // Survivor-only launches (the shared block went to the tensor cores) have
   // no other CTAs to hide their L2 latency behind: 3-stage ring instead of 2.
   if (a.skip_shared)
@@ -547,7 +544,6 @@ static lsb_status launch_logits_survivors(lsb_ctx* ctx, LogitsArgs a, lsb_mode m
   // 116 us; TMA bulk row copies 129 us (the per-lane operands serialise);
   // shared block in 16-row 4x4 tiles at 4 CTAs/SM 141 us; 3x2 lanes at 8
   // CTAs/SM 150 us.
-  static const bool one_d = getenv("LSB_K4_1D") != nullptr;
   // Small batches (a few sentences) fill a fraction of the GPU and each CTA
   // waits on its chunk loads: 32-column tiles (4x the CTAs) and an 8-deep ring.
   // (Measured, cfg 2 shapes: S=1 36 -> 18 us, S=8 49 -> 29, S=16 66 -> 49,
@@ -566,17 +562,14 @@ static lsb_status launch_logits_survivors(lsb_ctx* ctx, LogitsArgs a, lsb_mode m
                                                  : est <= 2L * ctx->sm_count);
 #define LSB_RB2(R)                                                                   \
   case R:                                                                            \
-    if (!one_d && small && a.skip_shared) /* survivors beside the TC block: */       \
+    if (small && a.skip_shared) /* survivors beside the TC block */                  \
       return fast ? launch_logits_rb<R, 2, false, 32, true, 4>(ctx, a, target_ctas)  \
                   : launch_logits_rb<R, 2, true, 32, true, 4>(ctx, a, target_ctas);  \
-    if (!one_d && small)                                                             \
+    if (small)                                                                       \
       return fast ? launch_logits_rb<R, 1, false, 32, true, 8>(ctx, a, target_ctas)  \
                   : launch_logits_rb<R, 1, true, 32, true, 8>(ctx, a, target_ctas);  \
-    if (!one_d)                                                                      \
-      return fast ? launch_logits_rb<R, 4, false, 32, true>(ctx, a, target_ctas)     \
-                  : launch_logits_rb<R, 4, true, 32, true>(ctx, a, target_ctas);     \
-    return fast ? launch_logits_rb<R, 1, false>(ctx, a, target_ctas)                 \
-                : launch_logits_rb<R, 1, true>(ctx, a, target_ctas);
+    return fast ? launch_logits_rb<R, 4, false, 32, true>(ctx, a, target_ctas)       \
+                : launch_logits_rb<R, 4, true, 32, true>(ctx, a, target_ctas);
   switch (rb) {
     LSB_RB2(16)
     LSB_RB2(12)
