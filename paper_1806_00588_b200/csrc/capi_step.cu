@@ -358,8 +358,15 @@ lsb_status lsb_step_host(lsb_batch* b, const lsb_state_host* in, lsb_choice* cho
     LSB_CUDA(dalloc(&b->h_nhyp, b->S));
     LSB_CUDA(dalloc(&b->h_choices, SB));
     LSB_CUDA(dalloc(&b->h_nchoices, b->S));
+    // rows past n_choices[s] are never written; zero them once so the
+    // whole-buffer read-back copies defined bytes
+    LSB_CUDA(cudaMemsetAsync(b->h_choices, 0, SB * sizeof(lsb_choice), st));
   }
-  if (hidden_out_host && !b->h_hidden_out) LSB_CUDA(dalloc(&b->h_hidden_out, HD));
+  if (hidden_out_host && !b->h_hidden_out) {
+    LSB_CUDA(dalloc(&b->h_hidden_out, HD));
+    // rows past n_choices[s] are not written by the reorder (see h_choices)
+    LSB_CUDA(cudaMemsetAsync(b->h_hidden_out, 0, HD * 4, st));
+  }
   LSB_CUDA(cudaMemcpyAsync(b->h_hidden, in->hidden, HD * 4, cudaMemcpyHostToDevice, st));
   LSB_CUDA(cudaMemcpyAsync(b->h_scores, in->scores, SB * 8, cudaMemcpyHostToDevice, st));
   lsb_state_dev d{};
@@ -409,6 +416,7 @@ lsb_status lsb_step_host_async(lsb_batch* b, const lsb_state_host* in, lsb_choic
       LSB_CUDA(dalloc(&sl.n_hyp, b->S));
       LSB_CUDA(dalloc(&sl.choices, SB));
       LSB_CUDA(dalloc(&sl.n_choices, b->S));
+      LSB_CUDA(cudaMemset(sl.choices, 0, SB * sizeof(lsb_choice)));
       LSB_CUDA(cudaEventCreateWithFlags(&sl.uploaded, cudaEventDisableTiming));
       LSB_CUDA(cudaEventCreateWithFlags(&sl.consumed, cudaEventDisableTiming));
       LSB_CUDA(cudaEventCreateWithFlags(&sl.computed, cudaEventDisableTiming));

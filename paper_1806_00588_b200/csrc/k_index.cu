@@ -682,6 +682,9 @@ lsb_status lsb_wta_hash(lsb_ctx* ctx, const float* M_host, int64_t n, int d,
   LSB_CUDA(cudaMemcpyAsync(p.p, perms_host, P * K * 4, cudaMemcpyHostToDevice, ctx->stream));
   st = launch_wta_hash(ctx, M.p, n, d, p.p, K, u, W, out.p);
   if (st) return st;
+  // a NaN row raises (invalid_argument) before anything is copied back, so
+  // codes_host is left untouched as by the reference's throw
+  if ((st = lsb_ctx_sync(ctx))) return st;
   LSB_CUDA(cudaMemcpyAsync(codes_host, out.p, static_cast<size_t>(n) * W * 4,
                            cudaMemcpyDeviceToHost, ctx->stream));
   return lsb_ctx_sync(ctx);
