@@ -399,6 +399,27 @@ def run_extras(ctx, model, idx, Hd, sc, fin, nh, choices, nchoice, hout, args, l
         total += same.numel()
     out["fast_vs_parity_choice_agreement"] = {"agree": agree, "total": total,
                                               "frac": round(agree / max(total, 1), 6)}
+    # recall@B vs full (SURVEY §8 d): per row, the fraction of the exact
+    # full-vocabulary top-B logits (+bias) that the LSH candidate set holds,
+    # on the first 4 step inputs. The candidate sets are the reference's own
+    # (bit-exact), so this is the reference's recall on the same inputs; for
+    # iid random E and H it is near chance (the paper's recall needs trained
+    # embeddings; the reference's operating point is acceptance criterion 5).
+    from paper_1806_00588_b200.lshbeam import exact_topb
+    import numpy as np
+    hits = rows = 0
+    for k in range(4):
+        bp.step(base + k * step_bytes, sc, fin, nh, choices, nchoice, hout)
+        ctx.sync()
+        ids_exact, _ = exact_topb(ctx, model, base + k * step_bytes, S * B, B, bias=True)
+        for s_ in range(S):
+            cand = bp.candidates(s_)[0]
+            ex = ids_exact[s_ * B:(s_ + 1) * B]
+            hits += int(np.isin(ex, cand).sum())
+            rows += B
+    out["recall_at_B"] = {"value": round(hits / max(rows * B, 1), 4), "rows": rows,
+                          "note": "exact full-vocab top-B vs V_LSH, 4 inputs x 768 rows; "
+                                  "iid synthetic data: near chance, same as the reference"}
     for bb in {id(bp): bp, id(bf): bf, id(b): b}.values():
         bb.close()
     return out
