@@ -455,7 +455,7 @@ static lsb_status launch_logits_rb(lsb_ctx* ctx, LogitsArgs a, int target) {
     // at least 4 CTAs per row group: a large shared block must not leave each
     // sentence's ~3 survivor tiles to one CTA in series (S=128: 283 -> see DESIGN)
     const int want = std::max(kMinSurvivorCtas, (target - a.jobs_shared) / std::max(1, a.S * a.G));
-    a.X = static_cast<int>(std::min<size_t>({static_cast<size_t>(want), size_t(64), max_tiles}));
+    a.X = static_cast<int>(std::min<size_t>({static_cast<size_t>(want), size_t(512), max_tiles}));
   } else {
     a.X = 0;
   }
