@@ -44,8 +44,10 @@ typedef enum lsb_status {
  *          lanes, no FMA; src/beam_decoder.cpp:34-42 as compiled by GCC -O3),
  *          so logits, probabilities and chosen ids are bit-identical to the
  *          CPU reference.
- *  FAST:   FP32 FFMA in tile order; |dlogit| <= 1e-4 (1+|l|), ids exact
- *          except at near-ties. */
+ *  FAST:   tcgen05 tensor cores (3xTF32, fp32 accumulation) for the dense
+ *          part -- the top-T block shared by >= 256 rows, or the whole
+ *          vocabulary -- and paired FP32 FFMA for the rest;
+ *          |dlogit| <= 1e-4 (1+|l|), ids exact except at near-ties. */
 typedef enum lsb_mode { LSB_MODE_PARITY = 0, LSB_MODE_FAST = 1 } lsb_mode;
 
 /* One beam continuation, layout-compatible with lshbeam::BeamChoice
