@@ -4,7 +4,8 @@
   python scripts/ncu_summary.py gpurun_out/<tag> <tag>
 
 Writes
-  profiles/<tag>_launches.md   per-kernel share of the ncu launch list
+  profiles/<tag>_launches.md   per-kernel share of the ncu launch list (and
+                               <tag>_fast_launches.md for the FAST-mode list)
                                (gpu__time_duration.sum, cold-cache, serialised)
   profiles/<tag>_ncu_full.md   key `ncu --set full` metrics per captured kernel
   profiles/ncu_summary.json    the same metrics, read by bench.py for
@@ -87,19 +88,21 @@ def full_metrics(rep: str):
 def main():
     src, tag = sys.argv[1], sys.argv[2]
     os.makedirs(PROF, exist_ok=True)
-    lines = []
-    lf = os.path.join(src, "launches.csv")
-    if os.path.exists(lf):
+    for csv_name, out_name, extra in (("launches.csv", "launches", ""),
+                                      ("launches_fast.csv", "fast_launches", " --mode fast")):
+        lf = os.path.join(src, csv_name)
+        if not os.path.exists(lf):
+            continue
         t = launches(lf)
         tot = sum(sum(v) for v in t.values())
-        lines += [f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none)", "",
-                  "Cold-cache, serialised replay of `python bench.py --steps 20 --warmup 3 "
-                  "--no-cpu-baseline --no-extras`; compare shares, not absolutes.", "",
-                  "| kernel | launches | avg us | share |", "|---|---|---|---|"]
+        lines = [f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none)", "",
+                 "Cold-cache, serialised replay of `python bench.py --steps 20 --warmup 3 "
+                 f"--no-cpu-baseline --no-extras{extra}`; compare shares, not absolutes.", "",
+                 "| kernel | launches | avg us | share |", "|---|---|---|---|"]
         for k, v in sorted(t.items(), key=lambda x: -sum(x[1])):
             lines.append(f"| `{k}` | {len(v)} | {sum(v) / len(v):.2f} | "
                          f"{100 * sum(v) / tot:.1f}% |")
-        open(os.path.join(PROF, f"{tag}_launches.md"), "w").write("\n".join(lines) + "\n")
+        open(os.path.join(PROF, f"{tag}_{out_name}.md"), "w").write("\n".join(lines) + "\n")
     summ_path = os.path.join(PROF, "ncu_summary.json")
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
     md = [f"# {tag}: `ncu --set full` captures", ""]
