@@ -546,7 +546,7 @@ static lsb_status launch_logits_survivors(lsb_ctx* ctx, LogitsArgs a, lsb_mode m
   // CTAs/SM 150 us; output halves (reference lanes 0-1 / 2-3) in neighbouring
   // lanes, 3x8 half-outputs per lane with 8-byte loads (22 instead of 28
   // wavefronts per 48 FFMA2, bit-exact) 105 us; 3x2 lanes (64-column tiles) at
-  // 5 CTAs/SM 125 us.
+  // 5 CTAs/SM 125 us; 16-float chunks in a 4-deep ring at 5 CTAs/SM 113 us.
   // Small batches (a few sentences) fill a fraction of the GPU and each CTA
   // waits on its chunk loads: 32-column tiles (4x the CTAs) and an 8-deep ring.
   // (Measured, cfg 2 shapes: S=1 36 -> 18 us, S=8 49 -> 29, S=16 66 -> 49,
