@@ -319,7 +319,9 @@ lsb_status lsb_index_import(lsb_ctx* ctx, uint32_t vocab, int W, const uint32_t*
 
 /* The recurrence of the synthetic scorer, h' = tanh(W_h h + W_e E[token])
  * (src/model_provider.cpp:83-102), on the device: FP32 in the reference's
- * 4-lane order without FMA, tanh evaluated in double and rounded. */
+ * 4-lane order without FMA, then glibc's tanhf algorithm restated with
+ * explicitly rounded single-precision operations (bit-identical to the
+ * reference's std::tanh(float); checked over all 2^32 inputs). */
 typedef struct lsb_recurrent lsb_recurrent;  /* device W_h, W_e (d x d)  */
 lsb_status lsb_recurrent_create(lsb_ctx* ctx, const float* wh_host, const float* we_host, int d,
                                 lsb_recurrent** out);

@@ -7,6 +7,7 @@ package does not load the library; constructing a ``Context`` does, and
 fails loudly if it was not built.
 """
 from .lshbeam import (EMPTY_CODE, FAST, PARITY, Batch, Context, Index, Model,  # noqa: F401
-                      bits_for)
+                      Recurrent, bits_for, exact_topb)
 
-__all__ = ["Context", "Model", "Index", "Batch", "PARITY", "FAST", "EMPTY_CODE", "bits_for"]
+__all__ = ["Context", "Model", "Index", "Batch", "Recurrent", "PARITY", "FAST", "EMPTY_CODE",
+           "bits_for", "exact_topb"]

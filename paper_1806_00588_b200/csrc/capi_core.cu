@@ -4,6 +4,8 @@
 #include <string>
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "lsb_internal.cuh"
 
@@ -16,6 +18,24 @@ void set_error(const std::string& msg) { g_last_error = msg; }
 lsb_status cuda_status(cudaError_t e, const char* what) {
   set_error(std::string(what) + ": " + cudaGetErrorString(e));
   return e == cudaErrorMemoryAllocation ? LSB_ENOMEM : LSB_ECUDA;
+}
+
+lsb_status ensure_smem(const lsb_ctx* ctx, const void* func, size_t bytes) {
+  if (bytes <= 48 * 1024) return LSB_OK;  // the default limit
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> configured;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = configured[{func, ctx->device}];
+  if (bytes <= have) return LSB_OK;
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != ctx->device) LSB_CUDA(cudaSetDevice(ctx->device));
+  const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(bytes));
+  if (cur >= 0 && cur != ctx->device) cudaSetDevice(cur);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(max dynamic smem)");
+  have = bytes;
+  return LSB_OK;
 }
 
 }  // namespace lsb

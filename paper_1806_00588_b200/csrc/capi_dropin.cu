@@ -13,6 +13,7 @@
 #include <cstring>
 #include <vector>
 
+#include "glibc_tanhf.cuh"
 #include "k_step.cuh"
 
 namespace lsb {
@@ -96,8 +97,126 @@ __global__ void k_recurrence(const float* __restrict__ wh, const float* __restri
       acc = __fadd_rn(acc, l1);
       acc = __fadd_rn(acc, l2);
       acc = __fadd_rn(acc, l3);
-      o[r] = static_cast<float>(tanh(static_cast<double>(acc)));
+      o[r] = lsb_tanhf::tanhf(acc);  // glibc tanhf, bit for bit (glibc_tanhf.cuh)
     }
+  }
+}
+
+
+// ------------------------------------------------------- exact top-b
+// Order-preserving unsigned key of a float: larger float -> larger key; -0 and
+// +0 share a key (the reference compares with !=, so they tie and the smaller
+// id wins, src/eval_oracle.cpp:29-32).
+__device__ __forceinline__ uint32_t ordered_key(float x) {
+  uint32_t u = __float_as_uint(x);
+  if ((u & 0x7fffffffu) == 0) u = 0;
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// One CTA per row: radix select of the b-th largest key (4 passes of 8-bit
+// digits over the row, which stays in L2), then the entries above it plus the
+// smallest-index entries equal to it, ranked by (value desc, index asc).
+// Works for any sign (exact_topb runs on raw logits).
+constexpr int kTopbThreads = 512;
+__global__ void __launch_bounds__(kTopbThreads) k_exact_topb(const float* __restrict__ L,
+                                                             size_t ld, uint32_t n, int b,
+                                                             uint32_t* __restrict__ ids,
+                                                             float* __restrict__ vals) {
+  __shared__ uint32_t hist[256];
+  __shared__ uint32_t s_prefix, s_mask, s_above, s_need;
+  __shared__ uint32_t wsum[33];
+  __shared__ uint32_t sel_key[64], sel_col[64];
+  __shared__ uint32_t s_nsel;
+  const float* row = L + static_cast<size_t>(blockIdx.x) * ld;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_prefix = 0;
+    s_mask = 0;
+    s_above = 0;  // entries known to be above the selected prefix
+    s_need = b;   // rank (1-based) still to locate inside the prefix bucket
+    s_nsel = 0;
+  }
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int k = tid; k < 256; k += blockDim.x) hist[k] = 0;
+    __syncthreads();
+    const uint32_t prefix = s_prefix, mask = s_mask;
+    for (uint32_t c = tid; c < n; c += blockDim.x) {
+      const uint32_t key = ordered_key(__ldg(row + c));
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      // walk digits from the top until the need-th largest is inside
+      uint32_t need = s_need, acc = 0;
+      int dg = 255;
+      for (; dg > 0; --dg) {
+        if (acc + hist[dg] >= need) break;
+        acc += hist[dg];
+      }
+      s_need = need - acc;
+      s_above += acc;
+      s_prefix = prefix | (static_cast<uint32_t>(dg) << shift);
+      s_mask = mask | (255u << shift);
+    }
+    __syncthreads();
+  }
+  const uint32_t tau = s_prefix;     // the b-th largest key
+  const uint32_t take_eq = s_need;   // how many entries equal to tau are kept
+  // entries above tau (fewer than b of them, any order)
+  for (uint32_t c = tid; c < n; c += blockDim.x) {
+    const uint32_t key = ordered_key(__ldg(row + c));
+    if (key > tau) {
+      const uint32_t at = atomicAdd(&s_nsel, 1u);
+      sel_key[at] = key;
+      sel_col[at] = c;
+    }
+  }
+  // entries equal to tau: the take_eq smallest columns, by a block scan over
+  // contiguous per-thread column ranges
+  const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
+  const uint32_t c0 = min(n, tid * per), c1 = min(n, c0 + per);
+  uint32_t eq = 0;
+  for (uint32_t c = c0; c < c1; ++c) eq += ordered_key(__ldg(row + c)) == tau;
+  __syncthreads();
+  const uint32_t base_sel = s_nsel;
+  // block exclusive scan of eq (per-thread column ranges are in thread order)
+  const int lane = tid & 31, warp = tid >> 5;
+  uint32_t incl = eq;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    uint32_t w = lane < nw ? wsum[lane] : 0u, wi = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += v;
+    }
+    if (lane < nw) wsum[lane] = wi - w;
+  }
+  __syncthreads();
+  uint32_t ex = wsum[warp] + incl - eq;
+  for (uint32_t c = c0; c < c1 && ex < take_eq; ++c) {
+    if (ordered_key(__ldg(row + c)) == tau) {
+      sel_key[base_sel + ex] = tau;
+      sel_col[base_sel + ex] = c;
+      ++ex;
+    }
+  }
+  __syncthreads();
+  // rank the b selected entries: key desc, column asc
+  if (tid < b) {
+    const uint32_t k = sel_key[tid], c = sel_col[tid];
+    int rank = 0;
+    for (int j = 0; j < b; ++j) {
+      const uint32_t kj = sel_key[j], cj = sel_col[j];
+      rank += (kj > k) || (kj == k && cj < c);
+    }
+    ids[static_cast<size_t>(blockIdx.x) * b + rank] = c;
+    vals[static_cast<size_t>(blockIdx.x) * b + rank] = __ldg(row + c);
   }
 }
 
@@ -217,7 +336,7 @@ lsb_status lsb_cuckoo_build(lsb_ctx* ctx, const uint32_t* keys, const uint32_t* 
 
 lsb_status lsb_wta_indices(lsb_ctx* ctx, const float* M_host, int64_t n, int d,
                            const uint32_t* perms_host, int P, int K, uint32_t* idx_host) {
-  if (!ctx || n < 0 || d < 1 || P < 1 || K < 1 || K > 256)
+  if (!ctx || n < 0 || d < 1 || P < 1 || K < 1 || K > 65536)
     return set_error("wta_hash_vector: bad arguments"), LSB_EINVAL;
   if (d < K) return set_error("PermutationSet: dimension smaller than window"), LSB_EINVAL;
   for (size_t i = 0; i < static_cast<size_t>(P) * K; ++i)
@@ -369,12 +488,7 @@ lsb_status lsb_recurrence(lsb_ctx* ctx, const lsb_model* model, const lsb_recurr
   const int d = model->d;
   const size_t smem = static_cast<size_t>(d) * 8;
   if (smem > ctx->smem_optin) return set_error("lsb_recurrence: dimension too large"), LSB_EINVAL;
-  static size_t configured = 0;
-  if (smem > configured) {
-    LSB_CUDA(cudaFuncSetAttribute(k_recurrence, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    configured = smem;
-  }
+  if (lsb_status rc = ensure_smem(ctx, k_recurrence, smem)) return rc;
   const int threads = 256;
   const int gx = std::max(1, std::min((d + 7) / 8, 64));
   k_recurrence<<<dim3(gx, n), threads, smem, ctx->stream>>>(rec->wh, rec->we, model->E, model->V,
@@ -408,7 +522,7 @@ lsb_status lsb_step_hidden(lsb_ctx* ctx, const lsb_model* model, const lsb_recur
 
 // exact_topb_logits(H . E^T + bias, b): per row the b largest logits, ties
 // to the smaller id (src/eval_oracle.cpp:11-40). PARITY logits (K4 over the
-// whole vocabulary), then the K5a selection on the raw values.
+// whole vocabulary), then k_exact_topb on the signed values.
 lsb_status lsb_exact_topb(lsb_ctx* ctx, const lsb_model* model, const float* H, int rows,
                           int H_on_device, int b, int add_bias, uint32_t* ids_host,
                           float* values_host) {
@@ -420,9 +534,8 @@ lsb_status lsb_exact_topb(lsb_ctx* ctx, const lsb_model* model, const float* H, 
   const int d = model->d;
   const uint32_t V = model->V;
   cudaStream_t st = ctx->stream;
-  Dev<float> Hd, L;
-  Dev<TopEntry> top;
-  Dev<int32_t> topn;
+  Dev<float> Hd, L, vals;
+  Dev<uint32_t> ids;
   const float* Hp = H;
   if (!H_on_device) {
     LSB_CUDA(Hd.alloc(static_cast<size_t>(rows) * d));
@@ -430,8 +543,8 @@ lsb_status lsb_exact_topb(lsb_ctx* ctx, const lsb_model* model, const float* H, 
     Hp = Hd.p;
   }
   LSB_CUDA(L.alloc(static_cast<size_t>(rows) * V));
-  LSB_CUDA(top.alloc(static_cast<size_t>(rows) * b));
-  LSB_CUDA(topn.alloc(rows));
+  LSB_CUDA(ids.alloc(static_cast<size_t>(rows) * b));
+  LSB_CUDA(vals.alloc(static_cast<size_t>(rows) * b));
   LogitsArgs la{};
   la.H = Hp;
   la.d = d;
@@ -444,27 +557,15 @@ lsb_status lsb_exact_topb(lsb_ctx* ctx, const lsb_model* model, const float* H, 
   la.ldo = V;
   lsb_status rc = launch_logits(ctx, la, LSB_MODE_PARITY, ctx->sm_count * 8);
   if (rc) return rc;
-  SoftmaxArgs sa{};
-  sa.logits = L.p;
-  sa.ldl = V;
-  sa.R_total = rows;
-  sa.Bsent = rows;
-  sa.topB = b;
-  sa.n_const = V;
-  sa.probs_in = 1;
-  sa.top = top.p;
-  sa.top_n = topn.p;
-  sa.err = ctx->err_dev;
-  if ((rc = launch_softmax(ctx, sa))) return rc;
-  std::vector<TopEntry> t(static_cast<size_t>(rows) * b);
-  LSB_CUDA(cudaMemcpyAsync(t.data(), top.p, t.size() * sizeof(TopEntry), cudaMemcpyDeviceToHost, st));
-  rc = lsb_ctx_sync(ctx);
-  if (rc) return rc;
-  for (size_t i = 0; i < t.size(); ++i) {
-    if (ids_host) ids_host[i] = t[i].r;
-    if (values_host) values_host[i] = t[i].p;
-  }
-  return LSB_OK;
+  k_exact_topb<<<rows, kTopbThreads, 0, st>>>(L.p, V, V, b, ids.p, vals.p);
+  LSB_LAUNCHED(ctx, "k_exact_topb");
+  if (ids_host)
+    LSB_CUDA(cudaMemcpyAsync(ids_host, ids.p, static_cast<size_t>(rows) * b * 4,
+                             cudaMemcpyDeviceToHost, st));
+  if (values_host)
+    LSB_CUDA(cudaMemcpyAsync(values_host, vals.p, static_cast<size_t>(rows) * b * 4,
+                             cudaMemcpyDeviceToHost, st));
+  return lsb_ctx_sync(ctx);
 }
 
 }  // extern "C"

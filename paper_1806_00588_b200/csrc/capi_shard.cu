@@ -251,12 +251,7 @@ lsb_status lsb_shard_phase3(lsb_batch* b, const lsb_state_dev* in, const double*
   const int Bp = b->B + kShardSlack;
   const size_t smem = static_cast<size_t>(G) * Bp * 8;
   if (smem > ctx->smem_optin) return set_error("lsb_shard_phase3: too many shards"), LSB_EINVAL;
-  static size_t configured = 0;
-  if (smem > configured) {
-    LSB_CUDA(cudaFuncSetAttribute(k_shard_combine, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    configured = smem;
-  }
+  if (lsb_status rc = ensure_smem(ctx, k_shard_combine, smem)) return rc;
   k_shard_combine<<<R, kShT, smem, ctx->stream>>>(allsum_dev, alltop_dev, G, R, Bp, b->B, b->B,
                                                    in->finished, in->n_hyp, b->top, b->top_n,
                                                    ctx->err_dev);

@@ -163,7 +163,8 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
   b->T = cfg->top_merge;
   b->t = cfg->threshold;
   b->mode = cfg->mode;
-  b->cmode = cfg->full_vocab ? 2 : (cfg->threshold == 0 ? 1 : 0);
+  // kTopOnly ignores t and scores [0,T) U specials (src/beam_decoder.cpp:189-199)
+  b->cmode = cfg->full_vocab ? 2 : (!cfg->top_only && cfg->threshold == 0 ? 1 : 0);
   b->n_shared = b->cmode ? V : b->T;
   b->ncap = (static_cast<size_t>(V) + 3) & ~size_t(3);
   b->nwords = (V + 31) / 32;

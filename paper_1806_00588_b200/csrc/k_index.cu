@@ -37,9 +37,9 @@ __global__ void k_wta_hash_rows(const float* __restrict__ M, long long n, int d,
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarp = blockDim.x >> 5;
   const int dpad = (d + 3) & ~3;
-  const size_t per_warp = (static_cast<size_t>(dpad) * 4 + P + 15) & ~size_t(15);
+  const size_t per_warp = (static_cast<size_t>(dpad) * 4 + 2 * P + 15) & ~size_t(15);
   float* row = reinterpret_cast<float*>(smem + warp * per_warp);
-  uint8_t* idx = reinterpret_cast<uint8_t*>(row + dpad);
+  uint16_t* idx = reinterpret_cast<uint16_t*>(row + dpad);  // K <= 65536
   const bool vec = (d & 3) == 0;
   for (long long r = static_cast<long long>(blockIdx.x) * nwarp + warp; r < n;
        r += static_cast<long long>(gridDim.x) * nwarp) {
@@ -76,7 +76,7 @@ __global__ void k_wta_hash_rows(const float* __restrict__ M, long long n, int d,
           best = k;
         }
       }
-      idx[p] = static_cast<uint8_t>(best);
+      idx[p] = static_cast<uint16_t>(best);
     }
     __syncwarp();
     for (int w = lane; w < W; w += 32) {
@@ -365,6 +365,8 @@ lsb_status check_wta_params(int K, int u, int W) {
   if (K < 2) return set_error("WtaParams: K must be >= 2"), LSB_EINVAL;
   if (u < 1) return set_error("WtaParams: u must be >= 1"), LSB_EINVAL;
   if (W < 1) return set_error("WtaParams: W must be >= 1"), LSB_EINVAL;
+  // the device keeps argmax indices in 16 bits (K <= d in practice)
+  if (K > 65536) return set_error("WtaParams: K above 65536 is not supported"), LSB_EINVAL;
   if (u * bits_for(K) >= 31)
     return set_error("WtaParams: packing overflow, u*ceil(log2(K)) = " +
                      std::to_string(u * bits_for(K)) +
@@ -379,7 +381,7 @@ lsb_status launch_wta_hash(lsb_ctx* ctx, const float* M, long long n, int d,
   if (n == 0) return LSB_OK;
   const int P = u * W;
   const int dpad = (d + 3) & ~3;
-  const size_t per_warp = (static_cast<size_t>(dpad) * 4 + P + 15) & ~size_t(15);
+  const size_t per_warp = (static_cast<size_t>(dpad) * 4 + 2 * P + 15) & ~size_t(15);
   const size_t budget = 96 * 1024;
   int warps = static_cast<int>(std::min<size_t>(8, std::max<size_t>(1, budget / per_warp)));
   const size_t smem = per_warp * warps;
@@ -387,9 +389,7 @@ lsb_status launch_wta_hash(lsb_ctx* ctx, const float* M, long long n, int d,
     set_error("wta_hash: row of dimension " + std::to_string(d) + " exceeds shared memory");
     return LSB_EINVAL;
   }
-  if (smem > 0)
-    LSB_CUDA(cudaFuncSetAttribute(k_wta_hash_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+  if (lsb_status rc = ensure_smem(ctx, k_wta_hash_rows, smem)) return rc;
   const long long blocks_needed = (n + warps - 1) / warps;
   const int grid = static_cast<int>(std::min<long long>(blocks_needed, ctx->sm_count * 16LL));
   k_wta_hash_rows<<<grid, warps * 32, smem, ctx->stream>>>(M, n, d, perms, K, u, W, bits_for(K),

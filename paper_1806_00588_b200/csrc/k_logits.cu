@@ -428,13 +428,8 @@ int choose_rb(int B) {
 template <int RB, int CB, bool PARITY, bool VEC, int NS, int KC = 32, bool TWO_D = false>
 static lsb_status launch_variant(lsb_ctx* ctx, const LogitsArgs& a, int grid) {
   constexpr size_t smem = logits_smem_bytes<RB, CB, NS, KC, TWO_D>();
-  static bool configured = false;
   auto* kern = k_logits<RB, CB, PARITY, VEC, NS, KC, TWO_D>;
-  if (!configured) {
-    LSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    configured = true;
-  }
+  if (lsb_status rc = ensure_smem(ctx, kern, smem)) return rc;
   LSB_CUDA(launch_pdl(ctx, kern, dim3(grid), dim3(kLT), smem, a));
   LSB_LAUNCHED(ctx, "k_logits");
   return LSB_OK;

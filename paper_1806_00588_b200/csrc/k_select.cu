@@ -1082,25 +1082,14 @@ lsb_status launch_expand(lsb_ctx* ctx, const ExpandArgs& a) {
     // large ones (cfg 3, B=50: 49 vs 61 us)
     const bool wide = a.topB <= 16;
     auto* kern = wide ? k_expand<1024> : k_expand<512>;
-    static size_t configured[2] = {0, 0};
-    if (rank_smem > configured[wide]) {
-      LSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(rank_smem)));
-      configured[wide] = rank_smem;
-    }
+    if (lsb_status rc = ensure_smem(ctx, kern, rank_smem)) return rc;
     LSB_CUDA(launch_pdl(ctx, kern, dim3(a.S), dim3(wide ? 1024 : 512), rank_smem, a));
     LSB_LAUNCHED(ctx, "k_expand");
     return LSB_OK;
   }
   const size_t smem = static_cast<size_t>(nl) * (8 + 8 + 4 + 4 + 4) + 16;
   if (smem > ctx->smem_optin) return set_error("expand: too many rows"), LSB_EINVAL;
-  static size_t configured = 0;
-  if (smem > configured) {
-    LSB_CUDA(cudaFuncSetAttribute(k_expand_tournament,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    configured = smem;
-  }
+  if (lsb_status rc = ensure_smem(ctx, k_expand_tournament, smem)) return rc;
   k_expand_tournament<<<a.S, 256, smem, ctx->stream>>>(a);
   LSB_LAUNCHED(ctx, "k_expand_tournament");
   return LSB_OK;

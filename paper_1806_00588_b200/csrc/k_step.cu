@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(
   uint32_t* codes = reinterpret_cast<uint32_t*>(h + dpad);
   uint32_t* sp_start = codes + ix.W;    // per band: span start (hit) ...
   uint32_t* sp_pre = sp_start + ix.W;   // ... and exclusive prefix of span lengths [W + 1]
-  uint8_t* idx = reinterpret_cast<uint8_t*>(sp_pre + ix.W + 1);
+  uint16_t* idx = reinterpret_cast<uint16_t*>(sp_pre + ix.W + 1);  // K <= 65536
 
   __shared__ BandMeta s_bands[kWarpBands];  // few-band path: probe metadata
   if (ix.W <= kWarpBands)
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(
           }
         }
       }
-      idx[p_own] = static_cast<uint8_t>(best);
+      idx[p_own] = static_cast<uint16_t>(best);
     }
   } else if (ix.K <= kMaxKReg) {
     // more permutations than threads (large W): each thread's permutation
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(
           }
         }
       }
-      idx[p] = static_cast<uint8_t>(best);
+      idx[p] = static_cast<uint16_t>(best);
     }
   } else {
     for (int p = threadIdx.x; p < ix.P; p += blockDim.x) {
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(
           best = k;
         }
       }
-      idx[p] = static_cast<uint8_t>(best);
+      idx[p] = static_cast<uint16_t>(best);
     }
   }
   __syncthreads();
@@ -301,7 +301,7 @@ lsb_status launch_probe(lsb_ctx* ctx, const ProbeArgs& a) {
       a.t <= 0 ? 0
       : a.levels >= 0 ? static_cast<size_t>(a.levels + 1) * (a.slice_len / 8)
                       : ((static_cast<size_t>(a.slice_len) * a.counter_bytes + 15) & ~size_t(15));
-  const size_t smem = cbytes + ((ix.d + 3) & ~3) * 4 + (3 * ix.W + 1) * 4 + ix.P + 16;
+  const size_t smem = cbytes + ((ix.d + 3) & ~3) * 4 + (3 * ix.W + 1) * 4 + 2 * ix.P + 16;
   if (smem > ctx->smem_optin) {
     set_error("probe: shared memory budget exceeded");
     return LSB_EINVAL;
@@ -313,13 +313,7 @@ lsb_status launch_probe(lsb_ctx* ctx, const ProbeArgs& a) {
   auto* kern = threads == 1024 ? k_probe_count<1024>
                : threads == 512 ? k_probe_count<512>
                                 : k_probe_count<256>;
-  static size_t configured[3] = {0, 0, 0};
-  const int ki = threads == 1024 ? 2 : threads == 512 ? 1 : 0;
-  if (smem > configured[ki]) {
-    LSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    configured[ki] = smem;
-  }
+  if (lsb_status rc = ensure_smem(ctx, kern, smem)) return rc;
   // bit-sliced counters need little shared memory: 256-thread CTAs, 6 per SM,
   // so a 768-row step runs in one wave; a grid smaller than the GPU gets
   // 1024-thread CTAs (more loads in flight per row)
@@ -457,12 +451,7 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
 lsb_status launch_compact(lsb_ctx* ctx, const CompactArgs& a, int S) {
   const size_t smem = static_cast<size_t>(a.nwords) * 4;
   if (smem > ctx->smem_optin) return set_error("compact: vocabulary too large"), LSB_EINVAL;
-  static size_t configured = 0;
-  if (smem > configured) {
-    LSB_CUDA(cudaFuncSetAttribute(k_compact, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    configured = smem;
-  }
+  if (lsb_status rc = ensure_smem(ctx, k_compact, smem)) return rc;
   LSB_CUDA(launch_pdl(ctx, k_compact, dim3(S), dim3(1024), smem, a));
   LSB_LAUNCHED(ctx, "k_compact");
   return LSB_OK;

@@ -294,12 +294,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_tc_logits(TcLogitsArgs a) {
 template <int N, int S, int P = kTcPromote>
 static lsb_status launch_tc_n(lsb_ctx* ctx, const TcLogitsArgs& a) {
   constexpr size_t smem = static_cast<size_t>(S) * (tc::kM * 256 + N * 256);
-  static bool configured = false;
-  if (!configured) {
-    LSB_CUDA(cudaFuncSetAttribute(k_tc_logits<N, S, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    configured = true;
-  }
+  if (lsb_status rc = ensure_smem(ctx, k_tc_logits<N, S, P>, smem)) return rc;
   // x = hypothesis-row tiles (launched fastest), y = candidate-column tiles:
   // the CTAs that share one E tile run back to back and hit it in L2
   dim3 grid((a.rows + N - 1) / N, (a.ncols + tc::kM - 1) / tc::kM);

@@ -12,6 +12,8 @@
 
 #include "lshbeam_b200.h"
 
+struct lsb_ctx;
+
 namespace lsb {
 
 // ------------------------------------------------------------- constants
@@ -47,6 +49,14 @@ struct IndexView {
 // ----------------------------------------------------------- host state
 void set_error(const std::string& msg);
 lsb_status cuda_status(cudaError_t e, const char* what);
+// Raises `func`'s dynamic shared-memory limit to at least `bytes` on the
+// context's device. cudaFuncSetAttribute is per device, so the configured size
+// is remembered per (kernel, device) under a lock (thread-safe, multi-GPU).
+lsb_status ensure_smem(const lsb_ctx* ctx, const void* func, size_t bytes);
+template <class F>
+lsb_status ensure_smem(const lsb_ctx* ctx, F* func, size_t bytes) {
+  return ensure_smem(ctx, reinterpret_cast<const void*>(func), bytes);
+}
 
 }  // namespace lsb
 

@@ -77,6 +77,12 @@ class Context:
     def launches(self) -> int:
         return int(self.lib.lsb_ctx_launch_count(self.h))
 
+    def set_parallel_cuckoo(self, on: bool = True):
+        """Cuckoo slot placement of later index builds: False = the
+        reference's insertion order (slots equal CuckooTable::build's), True =
+        parallel atomicExch placement (same lookups, different slots)."""
+        N.check(self.lib.lsb_ctx_set_parallel_cuckoo(self.h, int(on)))
+
     def close(self):
         if getattr(self, "h", None):
             self.lib.lsb_ctx_destroy(self.h)
@@ -203,6 +209,43 @@ def exact_topb(ctx: "Context", model: "Model", H, rows: int, b: int, bias: bool 
         N.check(ctx.lib.lsb_exact_topb(ctx.h, model.h, _p(Hh), rows, 0, b, int(bias), _p(ids),
                                        _p(vals)), "exact_topb")
     return ids, vals
+
+
+class Recurrent:
+    """Device W_h, W_e of the synthetic scorer (lsb_recurrent): the
+    recurrence h' = tanh(W_h h + W_e E[token]) (src/model_provider.cpp:83-102)."""
+
+    def __init__(self, ctx: "Context", wh, we):
+        self.ctx, self.lib = ctx, ctx.lib
+        wh, we = _f32(wh), _f32(we)
+        h = C.c_void_p()
+        N.check(self.lib.lsb_recurrent_create(ctx.h, _p(wh), _p(we), wh.shape[0], C.byref(h)),
+                "lsb_recurrent_create")
+        self.h, self.dim = h, wh.shape[0]
+
+    def step_hidden(self, model: "Model", h, token: int) -> np.ndarray:
+        """step_hidden(model, h, token) with host vectors."""
+        h = _f32(h)
+        out = np.zeros(self.dim, np.float32)
+        N.check(self.lib.lsb_step_hidden(self.ctx.h, model.h, self.h, _p(h), token, _p(out)),
+                "step_hidden")
+        return out
+
+    def step(self, model: "Model", hidden_in: int, tokens: int, n: int, hidden_out: int):
+        """n hypotheses on the device (pointers): tokens[k] < 0 copies the row."""
+        N.check(self.lib.lsb_recurrence(self.ctx.h, model.h, self.h, hidden_in, tokens, n,
+                                        hidden_out), "lsb_recurrence")
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.lsb_recurrent_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Model:
