@@ -111,6 +111,9 @@ struct ExpandArgs {
 lsb_status launch_probe(lsb_ctx* ctx, const ProbeArgs& a);
 lsb_status launch_compact(lsb_ctx* ctx, const CompactArgs& a, int S);
 lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_ctas);
+// PARITY lane-pair kernel (k_logits_lp.cu): applicability and launch.
+bool logits_lp_applies(const LogitsArgs& a);
+lsb_status launch_logits_lp(lsb_ctx* ctx, const LogitsArgs& a, int target_ctas);
 // Tensor-core (tcgen05, 3xTF32) logits for rows x identity columns
 // [col0, col0 + ncols) of E; FAST mode only.
 lsb_status launch_tc_logits(lsb_ctx* ctx, const float* H, int rows, const float* E,
