@@ -36,6 +36,13 @@ struct lsb_batch {
   float* tc_A = nullptr;        // FAST: pre-tiled E[0, n_shared) for tcgen05
   float* tc_H = nullptr;        // FAST: per-step tiled H
   int tc_N = 0;
+  // long rows (full vocabulary / t = 0): segmented K5a scratch
+  int seg_P = 0;
+  float* seg_max = nullptr;
+  double* seg_sum = nullptr;
+  lsb::TopEntry* seg_top = nullptr;
+  int32_t* seg_n = nullptr;
+  uint32_t* seg_count = nullptr;
   lsb::TopEntry* sh_top = nullptr;   // vocabulary-sharded step: local top-B'
   int32_t* sh_topn = nullptr;
   // staging for lsb_step_host

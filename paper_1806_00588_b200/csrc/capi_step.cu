@@ -28,7 +28,8 @@ lsb_status free_batch(lsb_batch* b) {
   void* ptrs[] = {b->specials, b->qcodes,   b->bitmap,     b->ids,          b->n_cand,
                   b->prov,     b->logits,   b->top,        b->top_n,        b->h_hidden,
                   b->h_scores, b->h_finished, b->h_nhyp,   b->h_choices,    b->h_nchoices,
-                  b->h_hidden_out, b->sh_top, b->sh_topn, b->tc_A, b->tc_H, b->arrive};
+                  b->h_hidden_out, b->sh_top, b->sh_topn, b->tc_A, b->tc_H, b->arrive,
+                  b->seg_max, b->seg_sum, b->seg_top, b->seg_n, b->seg_count};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& sl : b->slot) {
@@ -201,6 +202,19 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
   if (e == cudaSuccess) e = dalloc(&b->top_n, SB);
   if (e == cudaSuccess) e = dalloc(&b->arrive, b->S);
   if (e == cudaSuccess) e = cudaMemset(b->arrive, 0, b->S * sizeof(uint32_t));
+  // every row scores all V words (full vocabulary, t = 0): rows that long
+  // take the segmented K5a (one CTA per row segment)
+  static const bool seg_off = getenv("LSB_NO_SEG") != nullptr;
+  if (e == cudaSuccess && b->cmode != 0 && V >= 8192 && !seg_off) {
+    b->seg_P = seg_count(ctx, static_cast<int>(SB), V, b->B);
+    const size_t np = SB * b->seg_P;
+    e = dalloc(&b->seg_max, np);
+    if (e == cudaSuccess) e = dalloc(&b->seg_sum, np);
+    if (e == cudaSuccess) e = dalloc(&b->seg_top, np * b->B);
+    if (e == cudaSuccess) e = dalloc(&b->seg_n, np);
+    if (e == cudaSuccess) e = dalloc(&b->seg_count, SB);
+    if (e == cudaSuccess) e = cudaMemset(b->seg_count, 0, SB * sizeof(uint32_t));
+  }
   // FAST: the rows sharing [0, n_shared) form a dense contraction for the
   // tensor cores; E's block is split into 3xTF32 and tiled once, here
   const int R = b->S * b->B;
@@ -332,6 +346,19 @@ lsb_status lsb_step(lsb_batch* b, const lsb_state_dev* in, const lsb_out_dev* ou
   } else if (b->cmode == 0 && k5 == 1) {
     // warp per row over the whole GPU, then the per-sentence expansion
     if ((rc = launch_softmax_warp(ctx, sa, static_cast<uint32_t>(b->ncap)))) return rc;
+    if (b->rec) LSB_CUDA(cudaEventRecord(b->ev[4], st));
+    if ((rc = launch_expand(ctx, ea))) return rc;
+  } else if (b->seg_P > 0) {
+    SegArgs g{};
+    g.sa = sa;
+    g.P = b->seg_P;
+    g.seglen = static_cast<uint32_t>((b->V + b->seg_P - 1) / b->seg_P);
+    g.part_max = b->seg_max;
+    g.part_sum = b->seg_sum;
+    g.seg_top = b->seg_top;
+    g.seg_n = b->seg_n;
+    g.count = b->seg_count;
+    if ((rc = launch_softmax_seg(ctx, g))) return rc;
     if (b->rec) LSB_CUDA(cudaEventRecord(b->ev[4], st));
     if ((rc = launch_expand(ctx, ea))) return rc;
   } else {

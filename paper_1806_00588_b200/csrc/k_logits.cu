@@ -529,17 +529,15 @@ lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_c
 static lsb_status launch_logits_survivors(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode,
                                           int target_ctas) {
   const bool fast = mode == LSB_MODE_FAST;
-  // PARITY with enough work for a wave of 256-column lane-pair tiles: the
-  // FP32-issue-bound kernel of k_logits_lp.cu (same bits). Small batches keep
-  // the 32-column latency tiles below.
-  static const int lp_min_jobs = getenv("LSB_K4_LP_MIN") ? atoi(getenv("LSB_K4_LP_MIN")) : -1;
-  if (!fast && logits_lp_applies(a)) {
-    const long rg = (a.R_total + 11) / 12;
-    const long jobs = rg * ((a.skip_shared ? 0 : static_cast<long>(a.n_shared)) + 255) / 256 +
-                      (a.ids ? static_cast<long>(a.S) * 4 : 0);
-    if (jobs >= (lp_min_jobs >= 0 ? lp_min_jobs : ctx->sm_count))
-      return launch_logits_lp(ctx, a, target_ctas);
-  }
+  // PARITY over a large identity block shared by >= 2 row groups (the full
+  // vocabulary): the one-lane-per-thread kernel of k_logits_ln.cu (same bits;
+  // B200 cfg-2 shapes, S = 16 / 64 / 128: 588 / 2265 / 4606 us vs 633 / 2696 /
+  // 5328 us here). With per-sentence survivors it measured slower (108-125 vs
+  // 100 us at cfg 2), so the LSH step keeps the tiles below.
+  static const int ln_mode = getenv("LSB_K4_LN") ? atoi(getenv("LSB_K4_LN")) : 1;
+  if (!fast && ln_mode && logits_ln_applies(a) &&
+      (ln_mode == 2 || (!a.ids && a.R_total > 12 && a.n_shared >= 4096)))
+    return launch_logits_ln(ctx, a, target_ctas);
 #define LSB_RB(R)                                                        \
   case R:                                                                \
     return fast ? launch_logits_rb<R, 1, false>(ctx, a, target_ctas)     \

@@ -111,9 +111,9 @@ struct ExpandArgs {
 lsb_status launch_probe(lsb_ctx* ctx, const ProbeArgs& a);
 lsb_status launch_compact(lsb_ctx* ctx, const CompactArgs& a, int S);
 lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_ctas);
-// PARITY lane-pair kernel (k_logits_lp.cu): applicability and launch.
-bool logits_lp_applies(const LogitsArgs& a);
-lsb_status launch_logits_lp(lsb_ctx* ctx, const LogitsArgs& a, int target_ctas);
+// PARITY one-lane-per-thread kernel (k_logits_ln.cu): applicability and launch.
+bool logits_ln_applies(const LogitsArgs& a);
+lsb_status launch_logits_ln(lsb_ctx* ctx, const LogitsArgs& a, int target_ctas);
 // Tensor-core (tcgen05, 3xTF32) logits for rows x identity columns
 // [col0, col0 + ncols) of E; FAST mode only.
 lsb_status launch_tc_logits(lsb_ctx* ctx, const float* H, int rows, const float* E,
@@ -128,6 +128,20 @@ size_t tf32_tiled_floats(int nrows, int d, int R);
 int tc_rows_per_tile(lsb_ctx* ctx, int rows, uint32_t ncols);
 constexpr int kTcMinRows = 64;  // rows sharing a column block before tensor cores pay
 lsb_status launch_softmax(lsb_ctx* ctx, const SoftmaxArgs& a);
+// K5a for long rows (k_softmax_seg.cu): P segments per row, one CTA each.
+constexpr int kSegMaxP = 64;
+struct SegArgs {
+  SoftmaxArgs sa;
+  int P;
+  uint32_t seglen;
+  float* part_max;    // [R][P]
+  double* part_sum;   // [R][P]
+  TopEntry* seg_top;  // [R][P][topB]
+  int32_t* seg_n;     // [R][P]
+  uint32_t* count;    // [R], zero between steps (self-resetting)
+};
+int seg_count(lsb_ctx* ctx, int R, uint32_t n, int B);
+lsb_status launch_softmax_seg(lsb_ctx* ctx, const SegArgs& g);
 lsb_status launch_expand(lsb_ctx* ctx, const ExpandArgs& a);
 // Fused K5a+K5b (one launch; see k_select.cu) when select_fused_applies().
 bool select_fused_applies(const SoftmaxArgs& sa, const ExpandArgs& ea);

@@ -61,6 +61,9 @@ CASES = [
     (4000, 64, 4, 2, 8, 2, 24, 100, 1),
     # rows longer than the register path (n > 3072): global threshold path
     (8000, 64, 8, 3, 16, 2, 12, 4000, 2),
+    # t = 0 over V >= 8192: every row is the whole vocabulary -> segmented K5a
+    (9000, 32, 8, 3, 16, 2, 6, 0, 0),
+    (12000, 16, 4, 2, 8, 1, 40, 0, 0),
 ]
 
 
@@ -113,8 +116,14 @@ def test_step_config1_shape(ctx, oracle):
 
 
 @pytest.mark.parametrize("mode", [0, 1])
-def test_full_vocab_step(ctx, oracle, mode):
-    V, d, S, B = 3000, 64, 3, 6
+@pytest.mark.parametrize("V,d,S,B", [
+    (3000, 64, 3, 6),
+    # >= 2 row groups over a >= 4096-column identity block: the PARITY
+    # one-lane-per-thread kernel (k_logits_ln.cu), RT = 12 / 10 / 6
+    (6000, 64, 4, 12), (5000, 128, 3, 10), (4100, 40, 5, 6),
+    # V >= 8192: segmented K5a (P segments per row, last CTA merges)
+    (9000, 64, 1, 12), (20000, 32, 3, 8)])
+def test_full_vocab_step(ctx, oracle, mode, V, d, S, B):
     E = oracle.gaussian(11, V * d).reshape(V, d)
     bias = oracle.synth_model(V, d, 11, 8.0, want=("bias",))["bias"]
     state = make_state(oracle, S, B, d, seed=5, frozen_every=4)
@@ -130,6 +139,22 @@ def test_full_vocab_step(ctx, oracle, mode):
             np.testing.assert_array_equal(np.array([c[0] for c in res[s]]), ws)
         else:
             np.testing.assert_allclose(np.array([c[0] for c in res[s]]), ws, rtol=1e-5)
+
+
+def test_step_parity_under_lane_kernel():
+    """The LSH step with every PARITY logits launch forced onto the
+    one-lane-per-thread kernel (LSB_K4_LN=2: shared block + survivor jobs) is
+    bit-identical to the oracle, like the default tiles."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_step.py"), "-k",
+                        "test_step_matches_oracle or test_step_config1_shape"],
+                       env={**os.environ, "LSB_K4_LN": "2"}, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
 def test_step_nan_hidden_rejected(ctx, oracle):
