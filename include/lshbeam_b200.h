@@ -342,6 +342,10 @@ lsb_status lsb_exact_topb(lsb_ctx* ctx, const lsb_model* model, const float* H, 
                           int H_on_device, int b, int add_bias, uint32_t* ids_host,
                           float* values_host);
 
+/* Measured peak of the paired FP32 pipe (lane-ops/s, 2 per FMUL+FADD MAC as
+ * K4 PARITY issues them); bench.py's roofline denominator for K4. */
+lsb_status lsb_measure_fp32x2_peak(lsb_ctx* ctx, double* lane_ops_per_s);
+
 /* ---------------------------------- 8. vocabulary-sharded step (cfg 4)
  * One rank's share of a decode step when E is split by contiguous vocabulary
  * slices across ranks (the reference has no multi-device path; SURVEY
@@ -363,6 +367,12 @@ lsb_status lsb_shard_phase2(lsb_batch* b, const lsb_state_dev* in, const float* 
                             uint32_t word_base, double* rowsum_dev, lsb_shard_top* top_dev);
 lsb_status lsb_shard_phase3(lsb_batch* b, const lsb_state_dev* in, const double* allsum_dev,
                             const lsb_shard_top* alltop_dev, int G, const lsb_out_dev* out);
+/* The same with ONE gather after phase 2: each rank passes rowsum_dev = P
+ * and top_dev = (lsb_shard_top*)(P + S*B) of one buffer P of
+ * S*B*(1 + lsb_shard_width()) 8-byte words, and the ranks' buffers are
+ * gathered back to back (rank order) into packed_dev. */
+lsb_status lsb_shard_phase3_packed(lsb_batch* b, const lsb_state_dev* in, const void* packed_dev,
+                                   int G, const lsb_out_dev* out);
 
 #ifdef __cplusplus
 }

@@ -124,6 +124,7 @@ _SIGS = [
     ("lsb_recurrent_destroy", C.c_int, [VP]),
     ("lsb_recurrence", C.c_int, [VP, VP, VP, VP, VP, C.c_int, VP]),
     ("lsb_step_hidden", C.c_int, [VP, VP, VP, VP, U32, VP]),
+    ("lsb_measure_fp32x2_peak", C.c_int, [VP, C.POINTER(C.c_double)]),
     ("lsb_exact_topb", C.c_int, [VP, VP, VP, C.c_int, C.c_int, C.c_int, C.c_int, VP, VP]),
     # vocabulary-sharded step
     ("lsb_shard_width", C.c_int, [VP]),
@@ -131,6 +132,8 @@ _SIGS = [
     ("lsb_shard_phase2", C.c_int, [VP, C.POINTER(lsb_state_dev), VP, C.c_int, U32, VP, VP]),
     ("lsb_shard_phase3", C.c_int, [VP, C.POINTER(lsb_state_dev), VP, VP, C.c_int,
                                    C.POINTER(lsb_out_dev)]),
+    ("lsb_shard_phase3_packed", C.c_int, [VP, C.POINTER(lsb_state_dev), VP, C.c_int,
+                                          C.POINTER(lsb_out_dev)]),
 ]
 
 EXPORTED = [s[0] for s in _SIGS]

@@ -112,8 +112,12 @@ __global__ void k_shard_pack(const TopEntry* __restrict__ top, const int32_t* __
 
 // Phase 3 selection: per row, p = fl(e * inv) for the G*B' gathered entries,
 // top-B by (p desc, word asc) via ranks (entries are distinct words).
+// Rank g's sums start at allsum + g * rank_stride and its lists at
+// alltop + g * rank_stride (strides in 8-byte words: separate gathers use
+// R and R * Bp; the packed layout R + R * Bp for both).
 __global__ void __launch_bounds__(kShT) k_shard_combine(const double* __restrict__ allsum,
                                                         const lsb_shard_top* __restrict__ alltop,
+                                                        size_t sum_stride, size_t top_stride,
                                                         int G, int R, int Bp, int B, int Bsent,
                                                         const uint8_t* finished, const int32_t* n_hyp,
                                                         TopEntry* __restrict__ top,
@@ -129,7 +133,7 @@ __global__ void __launch_bounds__(kShT) k_shard_combine(const double* __restrict
     return;
   }
   double denom = 0.0;
-  for (int g = 0; g < G; ++g) denom += allsum[static_cast<size_t>(g) * R + row];  // rank order
+  for (int g = 0; g < G; ++g) denom += allsum[g * sum_stride + row];  // rank order
   if (!(denom > 0.0)) {
     if (threadIdx.x == 0) {
       atomicOr(err, kErrEmptyRow);
@@ -142,7 +146,7 @@ __global__ void __launch_bounds__(kShT) k_shard_combine(const double* __restrict
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
   for (int q = threadIdx.x; q < n; q += kShT) {
-    const lsb_shard_top t = alltop[(static_cast<size_t>(q / Bp) * R + row) * Bp + q % Bp];
+    const lsb_shard_top t = alltop[(q / Bp) * top_stride + static_cast<size_t>(row) * Bp + q % Bp];
     const bool ok = t.e >= 0.0f;
     sp[q] = ok ? __fmul_rn(t.e, inv) : -1.0f;
     sw[q] = t.word;
@@ -241,20 +245,18 @@ lsb_status lsb_shard_phase2(lsb_batch* b, const lsb_state_dev* in, const float* 
   return LSB_OK;
 }
 
-lsb_status lsb_shard_phase3(lsb_batch* b, const lsb_state_dev* in, const double* allsum_dev,
-                            const lsb_shard_top* alltop_dev, int G, const lsb_out_dev* out) {
-  if (!live_args(b, in) || !allsum_dev || !alltop_dev || G < 1 || !out || !out->choices ||
-      !out->n_choices)
-    return set_error("lsb_shard_phase3: bad arguments"), LSB_EINVAL;
+static lsb_status shard_phase3(lsb_batch* b, const lsb_state_dev* in, const double* allsum_dev,
+                               const lsb_shard_top* alltop_dev, size_t sum_stride,
+                               size_t top_stride, int G, const lsb_out_dev* out) {
   lsb_ctx* ctx = b->ctx;
   const int R = b->S * b->B;
   const int Bp = b->B + kShardSlack;
   const size_t smem = static_cast<size_t>(G) * Bp * 8;
   if (smem > ctx->smem_optin) return set_error("lsb_shard_phase3: too many shards"), LSB_EINVAL;
   if (lsb_status rc = ensure_smem(ctx, k_shard_combine, smem)) return rc;
-  k_shard_combine<<<R, kShT, smem, ctx->stream>>>(allsum_dev, alltop_dev, G, R, Bp, b->B, b->B,
-                                                   in->finished, in->n_hyp, b->top, b->top_n,
-                                                   ctx->err_dev);
+  k_shard_combine<<<R, kShT, smem, ctx->stream>>>(allsum_dev, alltop_dev, sum_stride, top_stride,
+                                                   G, R, Bp, b->B, b->B, in->finished, in->n_hyp,
+                                                   b->top, b->top_n, ctx->err_dev);
   LSB_LAUNCHED(ctx, "k_shard_combine");
   ExpandArgs ea{};
   ea.S = b->S;
@@ -273,6 +275,26 @@ lsb_status lsb_shard_phase3(lsb_batch* b, const lsb_state_dev* in, const double*
   ea.choices = out->choices;
   ea.n_choices = out->n_choices;
   return launch_expand(ctx, ea);
+}
+
+lsb_status lsb_shard_phase3(lsb_batch* b, const lsb_state_dev* in, const double* allsum_dev,
+                            const lsb_shard_top* alltop_dev, int G, const lsb_out_dev* out) {
+  if (!live_args(b, in) || !allsum_dev || !alltop_dev || G < 1 || !out || !out->choices ||
+      !out->n_choices)
+    return set_error("lsb_shard_phase3: bad arguments"), LSB_EINVAL;
+  const size_t R = static_cast<size_t>(b->S) * b->B;
+  return shard_phase3(b, in, allsum_dev, alltop_dev, R, R * (b->B + kShardSlack), G, out);
+}
+
+lsb_status lsb_shard_phase3_packed(lsb_batch* b, const lsb_state_dev* in, const void* packed_dev,
+                                   int G, const lsb_out_dev* out) {
+  if (!live_args(b, in) || !packed_dev || G < 1 || !out || !out->choices || !out->n_choices)
+    return set_error("lsb_shard_phase3_packed: bad arguments"), LSB_EINVAL;
+  const size_t R = static_cast<size_t>(b->S) * b->B;
+  const size_t stride = R + R * (b->B + kShardSlack);  // 8-byte words per rank
+  const double* sums = static_cast<const double*>(packed_dev);
+  return shard_phase3(b, in, sums, reinterpret_cast<const lsb_shard_top*>(sums + R), stride,
+                      stride, G, out);
 }
 
 }  // extern "C"

@@ -96,7 +96,7 @@ __device__ __forceinline__ int ln_hslot(int r, int k, int RT) {
 
 // One job's column tiles with a compile-time CTA shape: WR x WC warp tiles of
 // RT rows x 32 columns (RTT = WR RT rows, CTT = 32 WC columns per CTA tile).
-// Staging: thread tid copies E pieces (column tid/8 + 16 i, floats 4 (tid%8)..)
+// Staging: thread tid copies E pieces (column tid/8 + NT/8 i, floats 4 (tid%8)..)
 // and H elements (row tid/32 + 4 i, float tid%32) of every chunk. Columns past
 // the tile end and rows past the row limit copy a valid column / row instead
 // (their outputs are never stored and every output is independent), so the
@@ -111,9 +111,9 @@ __device__ __forceinline__ void ln_job(const LogitsArgs& a, float* sm, uint32_t*
   constexpr int NQ = RT / 4;        // row quads per thread
   constexpr int NP = (RT % 4) / 2;  // + a trailing row pair
   constexpr int NPE = CTT * (kLnKC / 4) / NT;  // E pieces per thread per chunk
-  constexpr int HRS = NT / kLnKC;              // H rows covered per pass (4)
+  constexpr int ECS = NT / (kLnKC / 4);        // columns covered per pass
+  constexpr int HRS = NT / kLnKC;              // H rows covered per pass
   constexpr int NPH = (RTT + HRS - 1) / HRS;   // H elements per thread per chunk
-  static_assert(HRS == 4, "H passes of 4 rows (one quad)");
   static_assert(NPE * NT == CTT * (kLnKC / 4), "whole pieces");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int j = lane & 3, cg = lane >> 2;
@@ -124,9 +124,9 @@ __device__ __forceinline__ void ln_job(const LogitsArgs& a, float* sm, uint32_t*
   const int ntiles = static_cast<int>((m + CTT - 1) / CTT);
   const int wcol = wc * 32;
   const int epart = tid & 7, ecol0 = tid >> 3;
-  // H: a warp writes rows 4 i + (lane & 3) x 8 consecutive k -> 32
-  // consecutive floats of the quad layout (conflict-free)
-  const int hk = tid >> 2, hr0 = tid & 3;
+  // H: with 128 threads a warp writes rows 4 i + (lane & 3) x 8 consecutive k
+  // -> 32 consecutive floats of the quad layout (conflict-free)
+  const int hk = tid / HRS, hr0 = tid % HRS;
   // H sources (rows clamped into [row0, rowlim)) and smem slots: fixed per job
   // (32-bit element offsets: the chunk's base pointer is uniform)
   uint32_t hsrc[NPH];
@@ -154,11 +154,11 @@ __device__ __forceinline__ void ln_job(const LogitsArgs& a, float* sm, uint32_t*
     uint32_t esrc[EREG ? NPE : 1];
     if constexpr (EREG) {
 #pragma unroll
-      for (int i = 0; i < NPE; ++i) esrc[i] = soff[ecol0 + 16 * i] + epart * 4;
+      for (int i = 0; i < NPE; ++i) esrc[i] = soff[ecol0 + ECS * i] + epart * 4;
     }
     auto eoff = [&](int i) -> uint32_t {
       if constexpr (EREG) return esrc[i];
-      else return soff[ecol0 + 16 * i] + epart * 4;
+      else return soff[ecol0 + ECS * i] + epart * 4;
     };
 
     auto load_chunk = [&](int stage, int kc) {
@@ -169,7 +169,7 @@ __device__ __forceinline__ void ln_job(const LogitsArgs& a, float* sm, uint32_t*
       const float* Hc = a.H + c0;
       if (c0 + kLnKC <= d) {
 #pragma unroll
-        for (int i = 0; i < NPE; ++i) ln_cp16(Es + 16 * i * kLnKS, Ec + eoff(i), 16);
+        for (int i = 0; i < NPE; ++i) ln_cp16(Es + ECS * i * kLnKS, Ec + eoff(i), 16);
 #pragma unroll
         for (int i = 0; i < NPH; ++i)
           if (NPH * HRS == RTT || hdst[i] >= 0) ln_cp4(Hs + hdst[i], Hc + hsrc[i], 4);
@@ -177,7 +177,7 @@ __device__ __forceinline__ void ln_job(const LogitsArgs& a, float* sm, uint32_t*
         const bool ein = c0 + epart * 4 < d, hin = c0 + hk < d;
 #pragma unroll
         for (int i = 0; i < NPE; ++i)
-          ln_cp16(Es + 16 * i * kLnKS, ein ? Ec + eoff(i) : a.E, ein ? 16 : 0);
+          ln_cp16(Es + ECS * i * kLnKS, ein ? Ec + eoff(i) : a.E, ein ? 16 : 0);
 #pragma unroll
         for (int i = 0; i < NPH; ++i)
           if (NPH * HRS == RTT || hdst[i] >= 0)
@@ -273,7 +273,7 @@ __device__ __forceinline__ void ln_job(const LogitsArgs& a, float* sm, uint32_t*
 }
 
 template <int RT, int NW, int WRS, int NS>
-__global__ void __launch_bounds__(NW * 32, RT == 12 ? 4 : 5) k_logits_ln(LogitsArgs a) {
+__global__ void __launch_bounds__(NW * 32, (RT == 12 ? 16 : 20) / NW) k_logits_ln(LogitsArgs a) {
   static_assert(RT % 2 == 0 && RT <= 12, "RT even, <= 12");
   static_assert(NW % WRS == 0, "whole warp columns");
   constexpr int CTMAX = NW * 32;
@@ -357,6 +357,9 @@ static lsb_status launch_ln_rt(lsb_ctx* ctx, const LogitsArgs& a, int target) {
   // rows sharing the identity block: stack two warp rows once there are more
   // rows than one warp tile holds (E chunk reused by 2 RT rows)
   const int wrs = wrs_env ? wrs_env : (a.R_total > RT ? 2 : 1);
+  // (one row group over a long identity block -- a one-sentence full-
+  // vocabulary step -- in 64-column CTAs with a 4-deep ring measured 70.7 us
+  // vs 67.6 for k_logits' 128-column tiles: FP-latency, not bytes in flight)
   return wrs >= 2 ? launch_ln<RT, 4, 2, 2>(ctx, a, target) : launch_ln<RT, 4, 1, 2>(ctx, a, target);
 }
 

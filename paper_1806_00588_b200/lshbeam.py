@@ -73,6 +73,13 @@ class Context:
     def sm_count(self) -> int:
         return self.lib.lsb_ctx_sm_count(self.h)
 
+    def fp32x2_peak(self) -> float:
+        """Measured paired-FP32 peak of this GPU in lane-ops/s (the K4 PARITY
+        roofline denominator; lsb_measure_fp32x2_peak)."""
+        v = C.c_double(0.0)
+        N.check(self.lib.lsb_measure_fp32x2_peak(self.h, C.byref(v)), "lsb_measure_fp32x2_peak")
+        return float(v.value)
+
     @property
     def launches(self) -> int:
         return int(self.lib.lsb_ctx_launch_count(self.h))

@@ -9,13 +9,14 @@ phases of include/lshbeam_b200.h §8 separated by two all-gathers over the
 ranks (NCCL over NVLink in production, gloo in the CPU tests):
 
   phase1 -> all_gather(row max)                       4 B per row per rank
-  phase2 -> all_gather(row exp-sum), all_gather(top-B' lists)
+  phase2 -> all_gather(row exp-sum + top-B' lists, one packed buffer)
                                                       8 + 8*B' B per row per rank
   phase3 -> identical choices + hidden reorder on every rank
 
 At S=64, B=12 that is 768 rows x 140 B ~ 105 KB per rank per step: the
-exchange is latency-bound, so it is two collectives per step, batched over
-all sentences. The reference has no multi-device path; results equal the
+exchange is latency-bound, so it is two collectives per step (the minimum
+for bit-exact probabilities: exp needs the global max first), batched over
+all sentences, the sums and lists travelling in one buffer. The reference has no multi-device path; results equal the
 unsharded step bit for bit in PARITY mode (tests/test_gpu_vocab_shard.py).
 """
 from __future__ import annotations
@@ -67,9 +68,11 @@ class VocabShard:
         R = S * B
         dev = torch.device("cuda", ctx.device)
         self.rowmax = torch.empty(R, dtype=torch.float32, device=dev)
-        self.rowsum = torch.empty(R, dtype=torch.float64, device=dev)
-        # lsb_shard_top is {float, uint32}: 8 bytes, carried as int64 words
-        self.top = torch.empty(R * self.width, dtype=torch.int64, device=dev)
+        # phase 2's outputs share one buffer (one gather): R row sums (double)
+        # then R x B' lsb_shard_top entries ({float, uint32}: 8-byte words)
+        self.packed = torch.empty(R * (1 + self.width), dtype=torch.int64, device=dev)
+        self.rowsum = self.packed[:R].view(torch.float64)
+        self.top = self.packed[R:]
 
     @staticmethod
     def _state(hidden, scores, finished, n_hyp):
@@ -92,6 +95,13 @@ class VocabShard:
                                           alltop.data_ptr(), G, C.byref(out)),
                 "lsb_shard_phase3")
 
+    def phase3_packed(self, st, allpacked, G: int, choices, n_choices, hidden_out=None):
+        out = N.lsb_out_dev(choices.data_ptr(), n_choices.data_ptr(),
+                            hidden_out.data_ptr() if hidden_out is not None else None)
+        N.check(self.lib.lsb_shard_phase3_packed(self.batch.h, C.byref(st), allpacked.data_ptr(),
+                                                 G, C.byref(out)),
+                "lsb_shard_phase3_packed")
+
     def close(self):
         for x in (self.batch, self.index, self.model):
             x.close()
@@ -99,11 +109,19 @@ class VocabShard:
 
 def _gather(x, G: int, group):
     """all_gather in rank order into a flat buffer (the layout gloo and NCCL
-    both accept), viewed as [G, *x.shape]."""
+    both accept), viewed as [G, *x.shape]. Under gloo (the CPU tests, or
+    ranks sharing one GPU) CUDA tensors travel through host copies."""
     import torch
     import torch.distributed as dist
-    out = torch.empty(G * x.numel(), dtype=x.dtype, device=x.device)
-    dist.all_gather_into_tensor(out, x.reshape(-1), group=group)
+    src = x.reshape(-1)
+    host = x.is_cuda and dist.get_backend(group) == "gloo"
+    if host:
+        torch.cuda.current_stream(x.device).synchronize()
+        src = src.cpu()
+    out = torch.empty(G * x.numel(), dtype=x.dtype, device=src.device)
+    dist.all_gather_into_tensor(out, src, group=group)
+    if host:
+        out = out.to(x.device)
     return out.view((G,) + tuple(x.shape))
 
 
@@ -119,9 +137,8 @@ def sharded_step(shard, hidden, scores, finished, n_hyp, choices, n_choices, hid
     shard.phase1(st)
     allmax = _gather(shard.rowmax, G, group)
     shard.phase2(st, allmax, G)
-    allsum = _gather(shard.rowsum, G, group)
-    alltop = _gather(shard.top, G, group)
-    shard.phase3(st, allsum, alltop, G, choices, n_choices, hidden_out)
+    allpacked = _gather(shard.packed, G, group)
+    shard.phase3_packed(st, allpacked, G, choices, n_choices, hidden_out)
 
 
 def local_sharded_step(shards, hidden, scores, finished, n_hyp, choices, n_choices,
@@ -138,7 +155,6 @@ def local_sharded_step(shards, hidden, scores, finished, n_hyp, choices, n_choic
     allmax = torch.stack([s.rowmax for s in shards])
     for s, st in zip(shards, sts):
         s.phase2(st, allmax, G)
-    allsum = torch.stack([s.rowsum for s in shards])
-    alltop = torch.stack([s.top for s in shards])
+    allpacked = torch.stack([s.packed for s in shards])
     for s, st in zip(shards, sts):
-        s.phase3(st, allsum, alltop, G, choices, n_choices, hidden_out)
+        s.phase3_packed(st, allpacked, G, choices, n_choices, hidden_out)

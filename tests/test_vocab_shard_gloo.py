@@ -89,6 +89,15 @@ class OracleShard:
             top[row, : len(order), 1] = ids[order] + self.v0
         self.rowsum = torch.from_numpy(rowsum)
         self.top = torch.from_numpy(top.reshape(-1).view(np.int64).copy())
+        # the one-gather layout of VocabShard.packed: R sums, then R x B' entries
+        self.packed = torch.cat([self.rowsum.view(torch.int64), self.top])
+
+    def phase3_packed(self, st, allpacked, G, choices, n_choices, hidden_out=None):
+        import torch
+        R = self.S * self.B
+        ap = allpacked.reshape(G, -1)
+        self.phase3(st, ap[:, :R].contiguous().view(torch.float64), ap[:, R:].contiguous(), G,
+                    choices, n_choices, hidden_out)
 
     def phase3(self, st, allsum, alltop, G, choices, n_choices, hidden_out=None):
         hidden, scores, finished, n_hyp = st
