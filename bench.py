@@ -1,22 +1,27 @@
 #!/usr/bin/env python
 """Benchmark of the per-step LSH beam-search hot path (BASELINE.json).
 
-Workload (BASELINE configs[1], "batched decode loop"): 64 sentences x B=12
-hypotheses per GPU, |V|=40000, d=1000, WTA K=8 u=3 W=16, T=1000, t=2,
-specials {V-1}; 50 distinct synthetic step inputs (torch.randn, seed 7) are
-cycled, so one "step" = one pass of the fused hot path (hash, cuckoo lookup,
-candidate union, reduced softmax, beam expansion + hidden reorder) over one
-batch of 64 sentences. Metric: decode steps/s = sentence-steps per second
-(softmax path + beam expansion, the reference's StageTimes::softmax_path() +
-beam_expansion, include/lshbeam/beam_decoder.hpp:66-73).
+Workloads (--workload, default cfg2 = BASELINE configs[1]):
+  cfg2  64 sentences x B=12 per GPU, |V|=40000, d=1000, WTA K=8 u=3 W=16,
+        T=1000, t=2, specials {V-1}; sentence-sharded, weak scaling
+  cfg3  B=50, 256 sentences in total split over the GPUs, |V|=40000,
+        d=1000; sentence-sharded, strong scaling (configs[2])
+  cfg4  |V|=200000, d=1024, B=12, 64 sentences; vocabulary-sharded over the
+        GPUs with the NCCL top-B merge (configs[3]), strong scaling
+One "step" = one pass of the fused hot path (hash, cuckoo lookup, candidate
+union, reduced softmax, beam expansion + hidden reorder) over one batch.
+Metric: decode steps/s = sentence-steps per second (softmax path + beam
+expansion: the reference's StageTimes::softmax_path() + beam_expansion,
+include/lshbeam/beam_decoder.hpp:66-73). Synthetic inputs (torch.randn,
+seed 7) cycled; inputs exceed L2.
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--workload cfg2|cfg3|cfg4]
+                  [--impl reference]
 
-Multi-GPU: one process per GPU (torchrun), sentences sharded across ranks
-(weak scaling: 64 sentences per rank, no data-path collective), timing is the
-max over ranks of the device-timed region. The reference arm times the
-reference's own CPU implementation (oracle/_ref, compiled from
-/root/reference's sources) on the host cores.
+Multi-GPU: one process per GPU (torchrun); timing = max over ranks of the
+device-timed region. The reference arm times the reference's own CPU
+implementation (oracle/_ref, compiled from /root/reference's sources) on the
+host cores.
 """
 from __future__ import annotations
 
@@ -31,9 +36,24 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CFG = dict(V=40000, d=1000, B=12, S=64, K=8, u=3, W=16, T=1000, t=2, seed=7, inputs=50)
 METRIC = "decode steps/sec (softmax+beam expand) at |V|=40k,d=1000,B=12; recall@B vs full"
 UNIT = "sentence-steps/s"
+
+WORKLOADS = {
+    "cfg2": dict(V=40000, d=1000, B=12, S=64, K=8, u=3, W=16, T=1000, t=2, seed=7, inputs=50,
+                 scaling="weak",
+                 desc="cfg2: batched decode step, 64 sentences x B=12 per GPU, |V|=40000, "
+                      "d=1000, K=8 u=3 W=16, T=1000, t=2"),
+    "cfg3": dict(V=40000, d=1000, B=50, S=256, K=8, u=3, W=16, T=1000, t=2, seed=7, inputs=6,
+                 scaling="strong",
+                 desc="cfg3: large beam B=50, 256 sentences split over the GPUs, |V|=40000, "
+                      "d=1000, K=8 u=3 W=16, T=1000, t=2"),
+    "cfg4": dict(V=200000, d=1024, B=12, S=64, K=8, u=3, W=16, T=1000, t=2, seed=7, inputs=8,
+                 scaling="strong",
+                 desc="cfg4: large vocabulary |V|=200000, d=1024, B=12, 64 sentences, "
+                      "vocabulary-sharded over the GPUs (NCCL top-B merge), K=8 u=3 W=16, "
+                      "T=1000, t=2"),
+}
 
 
 def parse():
@@ -42,9 +62,10 @@ def parse():
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     p.add_argument("--mode", default="parity", choices=["parity", "fast"])
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--no-extras", action="store_true", help="skip full-vocab / fast-mode lines")
+    p.add_argument("--no-extras", action="store_true", help="skip the same-GPU comparison legs")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     return p.parse_args()
 
@@ -56,18 +77,35 @@ def dist_info():
     return rank, world, local
 
 
-def make_inputs(rank: int):
+def sentences_per_rank(c, world):
+    return c["S"] if c["scaling"] == "weak" or c.get("vocab_sharded") else c["S"] // world
+
+
+def workload_config(name, world):
+    """The `config` object of the JSON line: identical in both arms."""
+    c = WORKLOADS[name]
+    par = {"cfg2": f"sentence-sharded x{world}", "cfg3": f"sentence-sharded x{world}",
+           "cfg4": f"vocabulary-sharded x{world}"}[name]
+    return {"workload": c["desc"], "sentences": c["S"] * (world if c["scaling"] == "weak" else 1),
+            "beam": c["B"], "vocab": c["V"], "dim": c["d"], "K": c["K"], "u": c["u"],
+            "W": c["W"], "T": c["T"], "t": c["t"], "specials": [c["V"] - 1],
+            "parallelism": par,
+            "l2": "inputs larger than L2 (E %d MB + cycled step inputs)" % (c["V"] * c["d"] * 4 >> 20)}
+
+
+def make_inputs(name, rank, world):
     """Synthetic inputs, identical in both arms: E ~ N(0,1) (seed 7), zero
-    bias; per rank 50 step inputs H ~ N(0,1) and cumulative
-    scores."""
+    bias; this rank's step inputs H ~ N(0,1) and cumulative
+    scores (rank-seeded for sentence sharding, shared for vocabulary sharding)."""
     import torch
-    c = CFG
+    c = WORKLOADS[name]
     g = torch.Generator().manual_seed(c["seed"])
     E = torch.randn(c["V"], c["d"], generator=g)
     bias = torch.zeros(c["V"])
-    g2 = torch.Generator().manual_seed(1000 + rank)
-    H = torch.randn(c["inputs"], c["S"], c["B"], c["d"], generator=g2)
-    scores = -torch.rand(c["S"], c["B"], generator=g2, dtype=torch.float64) * 4.0
+    S = sentences_per_rank(c, world)
+    g2 = torch.Generator().manual_seed(1000 + (0 if name == "cfg4" else rank))
+    H = torch.randn(c["inputs"], S, c["B"], c["d"], generator=g2)
+    scores = -torch.rand(S, c["B"], generator=g2, dtype=torch.float64) * 4.0
     return E, bias, H, scores
 
 
@@ -122,34 +160,52 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def measured_peak_hbm():
+def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return float(json.load(f)["hbm_gbs"]), "measured"
+            return json.load(f), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return 6650.0, "fallback"
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of k_logits from the committed ncu summary, if any."""
+def ncu_capture(kernel):
+    """Per-launch DRAM bytes of `kernel` from the committed ncu --set full
+    capture, with the capture's tag (the same binary and bench command)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            return json.load(f).get("k_logits", {}).get("dram_bytes_per_launch")
+            e = json.load(f).get(kernel, {})
+        return e.get("dram_bytes_per_launch"), e.get("tag")
     except Exception:
-        return None
+        return None, None
+
+
+def dev_timer(ctx):
+    import torch
+    st = torch.cuda.ExternalStream(ctx.stream)
+
+    def run(fn, steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for k in range(steps):
+            fn(k)
+        b.record(st)
+        b.synchronize()
+        ctx.sync()
+        return a.elapsed_time(b) / steps
+    return run
 
 
 # ----------------------------------------------------------------- ours
 def run_ours(args, rank, world, local):
-    import ctypes as C
-
     import numpy as np
     import torch
 
     from paper_1806_00588_b200 import FAST, PARITY, Batch, Context, Index, Model
-    from paper_1806_00588_b200 import _native as N
+    from paper_1806_00588_b200.seeds import mix_seed
 
-    c = CFG
+    name = args.workload
+    c = WORKLOADS[name]
+    vsh = name == "cfg4" and world > 1
     ngpu = torch.cuda.device_count()
     # one rank per GPU; more ranks than GPUs (a functional check on a small
     # box) share devices and time through gloo, since NCCL refuses that
@@ -162,22 +218,28 @@ def run_ours(args, rank, world, local):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")
-    E, bias, H, scores = make_inputs(rank)
+    E, bias, H, scores = make_inputs(name, rank, world)
+    S, B, d, V = H.shape[1], c["B"], c["d"], c["V"]
     stream = torch.cuda.Stream()
     ctx = Context(local, stream.cuda_stream)
-    Ed, bd = E.cuda(), bias.cuda()
-    torch.cuda.synchronize()
-    model = Model(ctx, None, device_ptrs=(Ed.data_ptr(), bd.data_ptr(), c["V"], c["d"]))
-    del Ed, bd
-    t0 = time.perf_counter()
-    from paper_1806_00588_b200.seeds import mix_seed
-    idx = Index(ctx, model, K=c["K"], u=c["u"], W=c["W"], perm_seed=mix_seed(c["seed"], 1),
-                index_seed=mix_seed(c["seed"], 2))
-    index_ms = (time.perf_counter() - t0) * 1e3
     mode = PARITY if args.mode == "parity" else FAST
-    S, B, d = c["S"], c["B"], c["d"]
-    batch = Batch(ctx, model, idx, S=S, B=B, T=c["T"], t=c["t"], specials=[c["V"] - 1],
-                  mode=mode)
+    ps, isd = mix_seed(c["seed"], 1), mix_seed(c["seed"], 2)
+    t0 = time.perf_counter()
+    if vsh:
+        from paper_1806_00588_b200.vocab_shard import VocabShard, shard_bounds, sharded_step
+        v0, n = shard_bounds(V, world, rank)
+        Es, bs = E[v0:v0 + n].cuda().contiguous(), bias[v0:v0 + n].cuda()
+        shard = VocabShard(ctx, Es, bs, v0, V, c["K"], c["u"], c["W"], ps, isd, S, B, c["T"],
+                           c["t"], specials=[V - 1], mode=mode)
+        model, idx, batch = shard.model, shard.index, shard.batch
+    else:
+        Ed, bd = E.cuda(), bias.cuda()
+        torch.cuda.synchronize()
+        model = Model(ctx, None, device_ptrs=(Ed.data_ptr(), bd.data_ptr(), V, d))
+        idx = Index(ctx, model, K=c["K"], u=c["u"], W=c["W"], perm_seed=ps, index_seed=isd)
+        batch = Batch(ctx, model, idx, S=S, B=B, T=c["T"], t=c["t"], specials=[V - 1], mode=mode)
+    ctx.sync()
+    index_ms = (time.perf_counter() - t0) * 1e3
     Hd = H.cuda()
     sc = scores.cuda()
     fin = torch.zeros(S, B, dtype=torch.uint8, device="cuda")
@@ -189,8 +251,13 @@ def run_ours(args, rank, world, local):
     base = Hd.data_ptr()
     torch.cuda.synchronize()
 
-    def step(k):
-        batch.step(base + (k % c["inputs"]) * step_bytes, sc, fin, nh, choices, nchoice, hout)
+    if vsh:
+        def step(k):
+            with torch.cuda.stream(stream):
+                sharded_step(shard, Hd[k % c["inputs"]], sc, fin, nh, choices, nchoice, hout)
+    else:
+        def step(k):
+            batch.step(base + (k % c["inputs"]) * step_bytes, sc, fin, nh, choices, nchoice, hout)
 
     # candidate counts per input (deterministic) for the algorithmic byte count
     ncand = np.zeros((c["inputs"], S), np.int64)
@@ -201,87 +268,137 @@ def run_ours(args, rank, world, local):
     for k in range(args.warmup):
         step(k)
     ctx.sync()
-    # stage events on every 8th step only: events between kernels would break
-    # programmatic dependent launch on the steps they separate
-    batch.profile(True, every=8)
     launches0 = ctx.launches
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        with torch.cuda.stream(stream):
-            start.record(stream)
-            for k in range(args.steps):
-                step(k)
-            end.record(stream)
+        start.record(stream)
+        for k in range(args.steps):
+            step(k)
+        end.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     ctx.sync()
     launches = ctx.launches - launches0
     ms = start.elapsed_time(end)
-    stage_tot, nrec = batch.stage_totals()
-    batch.profile(False)
     if world > 1:
         t = torch.tensor([ms], device=coll_dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    value = S * world * args.steps / (ms / 1e3)
+    S_job = c["S"] * (world if c["scaling"] == "weak" else 1)
+    value = S_job * args.steps / (ms / 1e3)
 
-    # dominant kernel: k_logits. Algorithmic bytes per launch = unique E rows
-    # (shared top-T block once + each sentence's survivors) + H + ids/bias +
-    # logits written.
-    used = ncand[np.arange(args.steps) % c["inputs"]]
-    m = np.maximum(used - c["T"], 0)
-    e_rows = c["T"] + m.sum(axis=1)
-    alg_bytes = (e_rows * d * 4 + S * B * d * 4 + (c["T"] + m.sum(axis=1)) * 8
-                 + B * used.sum(axis=1) * 4).mean()
-    flops = (2.0 * B * used.sum(axis=1) * d).mean()
-    logits_ms = float(stage_tot[2]) / max(nrec, 1)
-    peak, peak_kind = measured_peak_hbm()
-    achieved = alg_bytes / (logits_ms / 1e3) / 1e9
-    # The binding resource of K4 in PARITY is FP32 instruction issue, not HBM:
-    # every MAC is an FMUL + an FADD (no FMA, reference order). Peak lane-op
-    # rate = SMs x 128 FP32 lanes x SM clock (median under load).
-    macs = flops / 2.0
-    roofline = {"kernel": "k_logits", "bound": "hbm", "achieved": round(achieved, 1),
-                "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(),
-                "alg_bytes_per_launch": int(alg_bytes), "launch_ms": round(logits_ms, 5),
-                "launches_timed": int(nrec),
-                "macs_per_launch": int(macs),
-                "fp32_tflops": round(flops / (logits_ms / 1e3) / 1e12, 2),
-                "note": "PARITY: FMUL+FADD per MAC in the reference order as FFMA2 pairs; bound "
-                        "jointly by the FP32 pipe (fp32_issue) and shared-memory wavefronts "
-                        "(each 16-B LDS costs 4 wavefronts; ncu: ~60% of both)"
-                        if mode == PARITY else
-                        "FAST: paired FFMA2 chains (tcgen05 3xTF32 only for the full-vocabulary "
-                        "block)"}
+    # Per-stage device times from a separate instrumented pass (stage events
+    # between kernels would break programmatic dependent launch inside the
+    # timed region): 30 steps, every step instrumented.
+    batch.profile(True, every=1)
+    for k in range(30):
+        step(k)
+    stage_tot, nrec = batch.stage_totals()
+    batch.profile(False)
     stages = {k: round(float(v) / max(nrec, 1), 5) for k, v in
               zip(["probe_count", "compact", "logits", "softmax_topb", "expand"], stage_tot)}
 
+    # Dominant kernel: K4 (k_logits). Algorithmic work per launch: unique E
+    # rows (shared top-T block once + each sentence's survivors) + H + ids/bias
+    # + logits written; MACs = B x sum n x d (FMUL + FADD each in PARITY).
+    used = ncand[np.arange(args.steps) % c["inputs"]]
+    T_loc = c["T"]
+    if vsh:
+        from paper_1806_00588_b200.vocab_shard import local_config
+        T_loc = local_config(c["T"], [V - 1], v0, n)[0]
+    m = np.maximum(used - T_loc, 0)
+    alg_bytes = ((T_loc + m.sum(axis=1)) * d * 4 + S * B * d * 4 + (T_loc + m.sum(axis=1)) * 8
+                 + B * used.sum(axis=1) * 4).mean()
+    macs = float((B * used.sum(axis=1) * d).mean())
+    logits_ms = stages["logits"]
+    peaks, peak_src = measured_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_achieved = alg_bytes / (logits_ms / 1e3) / 1e9
+    fp32_peak = ctx.fp32x2_peak()  # lane-ops/s, measured now on this GPU
+    lane_ops = (2.0 if mode == PARITY else 1.0) * macs
+    fp32_achieved = lane_ops / (logits_ms / 1e3)
+    traffic, tag = ncu_capture("k_logits")
+    roofline = {
+        "kernel": "k_logits", "bound": "fp32",
+        "achieved": round(fp32_achieved / 1e12, 3), "peak": round(fp32_peak / 1e12, 3),
+        "unit": "T FP32 lane-ops/s", "frac": round(fp32_achieved / fp32_peak, 4),
+        "peak_kind": "measured in this run: lsb_measure_fp32x2_peak (paired FMUL+FADD, the "
+                     "instructions K4 PARITY issues), %d SMs" % ctx.sm_count,
+        "traffic": traffic, "traffic_capture": tag,
+        "launch_ms": round(logits_ms, 5), "launches_timed": int(nrec),
+        "macs_per_launch": int(macs), "lane_ops_per_launch": int(lane_ops),
+        "alg_bytes_per_launch": int(alg_bytes),
+        "hbm": {"achieved": round(hbm_achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(hbm_achieved / hbm_peak, 4), "peak_kind": peak_src},
+        "note": ("PARITY: one FMUL + one FADD per MAC in the reference's 4-lane order "
+                 "(bit-exact logits), issued as FFMA2 pairs: FP32-issue bound; the HBM "
+                 "fraction is reported beside it" if mode == PARITY else
+                 "FAST: FFMA2 chains / tcgen05 3xTF32 for the shared block")}
+
     # e2e: the public C-ABI call with host buffers (pinned), H2D + D2H inside
+    e2e = None
+    if not vsh:
+        e2e = time_e2e_leg(args, batch, H, scores, S, B, d, world, coll_dev, S_job)
+    else:
+        e2e = time_e2e_sharded(args, shard, sharded_step, H, scores, S, B, d, world, coll_dev,
+                               S_job, stream)
+
+    extras = {}
+    if not args.no_extras and rank == 0 and world == 1 and name == "cfg2":
+        extras = run_extras(ctx, model, idx, Hd, sc, fin, nh, choices, nchoice, hout, args,
+                            value, c)
+    line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
+            "higher_is_better": True, "scaling": c["scaling"], "vs_baseline": None,
+            "dtype": "f32", "mode": args.mode,
+            "data": "synthetic (torch.randn seed 7; E %dx%d fp32)" % (V, d),
+            "config": workload_config(name, world),
+            "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
+            "stage_ms": stages, "clocks": clk.summary(),
+            "run": {"batch_steps_per_s": round(1e3 / ms_per_step, 1),
+                    "sentences_per_rank": S, "mean_vlsh": float(used.mean()),
+                    "index_build_ms": round(index_ms, 1), "ranks_share_gpus": world > ngpu},
+            **extras}
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(name, E, bias, H, scores, args.cpu_seconds)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def time_e2e_leg(args, batch, H, scores, S, B, d, world, coll_dev, S_job):
+    """End to end through the public C ABI with pinned host buffers: every
+    step uploads its inputs and reads its choices back inside the timed
+    region (pipelined lsb_step_host_async, and synchronous lsb_step_host)."""
+    import ctypes as C
+
+    import torch
+    n_in = H.shape[0]
     Hh = H.pin_memory()
     sch = scores.pin_memory()
     finh = torch.zeros(S, B, dtype=torch.uint8).pin_memory()
     nhh = torch.full((S,), B, dtype=torch.int32).pin_memory()
     ch_h = torch.zeros(S * B * 24, dtype=torch.uint8).pin_memory()
     nc_h = torch.zeros(S, dtype=torch.int32).pin_memory()
-    hb = Hh.data_ptr()
-    chp = C.c_void_p(ch_h.data_ptr())
-    ncp = C.c_void_p(nc_h.data_ptr())
+    hb, step_bytes = Hh.data_ptr(), S * B * d * 4
+    chp, ncp = C.c_void_p(ch_h.data_ptr()), C.c_void_p(nc_h.data_ptr())
 
-    def step_e2e(k):
-        batch.step_host_ptrs(hb + (k % c["inputs"]) * step_bytes, sch.data_ptr(),
-                             finh.data_ptr(), nhh.data_ptr(), chp, ncp)
+    def sync_step(k):
+        batch.step_host_ptrs(hb + (k % n_in) * step_bytes, sch.data_ptr(), finh.data_ptr(),
+                             nhh.data_ptr(), chp, ncp)
 
-    def step_e2e_async(k):
-        batch.step_host_async(hb + (k % c["inputs"]) * step_bytes, sch.data_ptr(),
-                              finh.data_ptr(), nhh.data_ptr(), chp, ncp)
+    def async_step(k):
+        batch.step_host_async(hb + (k % n_in) * step_bytes, sch.data_ptr(), finh.data_ptr(),
+                              nhh.data_ptr(), chp, ncp)
 
-    def time_e2e(fn, finish):
+    def timed(fn, finish):
         for k in range(args.warmup):
             fn(k)
         finish()
@@ -300,93 +417,92 @@ def run_ours(args, rank, world, local):
             el = float(t.item())
         return el
 
-    # pipelined public API (step k+1's upload overlaps step k's kernels);
-    # every step still uploads its inputs from pinned host memory and reads
-    # its choices back into host memory inside the timed region
-    e2e_s = time_e2e(step_e2e_async, batch.wait)
-    e2e_sync_s = time_e2e(step_e2e, ctx.sync)
-    e2e = {"value": round(S * world * args.steps / e2e_s, 1), "unit": UNIT,
-           "h2d_bytes_per_step": S * B * d * 4 + S * B * 8 + S * B + S * 4,
-           "d2h_bytes_per_step": S * B * 24 + S * 4, "api": "lsb_step_host_async (C ABI)",
-           "synchronous_value": round(S * world * args.steps / e2e_sync_s, 1),
-           "synchronous_api": "lsb_step_host (C ABI, one host sync per step)"}
-
-    extras = {}
-    if not args.no_extras and rank == 0:
-        extras = run_extras(ctx, model, idx, Hd, sc, fin, nh, choices, nchoice, hout, args,
-                            value)
-    line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "mode": args.mode, "data": "synthetic (torch.randn seed 7; E 40000x1000 fp32)",
-            "config": {"workload": "cfg2: batched decode step, 64 sentences x B=12 per GPU, "
-                                   "|V|=40000, d=1000, K=8 u=3 W=16, T=1000, t=2",
-                       "sentences_per_gpu": S, "beam": B, "vocab": c["V"], "dim": d,
-                       "K": c["K"], "u": c["u"], "W": c["W"], "T": c["T"], "t": c["t"],
-                       "parallelism": f"sentence-sharded x{world}" + (f" on {ngpu} GPU(s), ranks share devices" if world > ngpu else ""),
-                       "l2": "inputs larger than L2: E 160 MB + 50 cycled H inputs 154 MB",
-                       "batch_steps_per_s": round(value / S / world, 1),
-                       "mean_vlsh": float(used.mean()), "index_build_ms": round(index_ms, 1)},
-            "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
-            "stage_ms": stages, "clocks": clk.summary(), **extras}
-    sm_mhz = line["clocks"].get("sm_mhz") or 1965.0
-    lane_ops = (2.0 if mode == PARITY else 1.0) * macs  # FMUL+FADD vs FFMA per MAC
-    peak_ops = ctx.sm_count * 128 * sm_mhz * 1e6
-    line["roofline"]["fp32_issue"] = {
-        "lane_ops_per_launch": int(lane_ops), "achieved_tops": round(lane_ops / (logits_ms / 1e3) / 1e12, 2),
-        "peak_tops": round(peak_ops / 1e12, 2), "frac": round(lane_ops / (logits_ms / 1e3) / peak_ops, 4),
-        "peak_basis": f"{ctx.sm_count} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (median SM clock "
-                      "in the timed region)"}
-    if rank == 0 and not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline(E, bias, H, scores, args.cpu_seconds)
-    if world > 1:
-        torch.distributed.barrier()
-        torch.distributed.destroy_process_group()
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+    e_async = timed(async_step, batch.wait)
+    e_sync = timed(sync_step, batch.ctx.sync)
+    return {"value": round(S_job * args.steps / e_async, 1), "unit": UNIT,
+            "h2d_bytes_per_step": S * B * d * 4 + S * B * 8 + S * B + S * 4,
+            "d2h_bytes_per_step": S * B * 24 + S * 4, "api": "lsb_step_host_async (C ABI)",
+            "synchronous_value": round(S_job * args.steps / e_sync, 1),
+            "synchronous_api": "lsb_step_host (C ABI, one host sync per step)"}
 
 
-def run_extras(ctx, model, idx, Hd, sc, fin, nh, choices, nchoice, hout, args, lsh_value):
-    """Same-GPU comparison lines: the full-vocabulary fused path (kFull) and the
-    LSH path in the other arithmetic mode."""
+def time_e2e_sharded(args, shard, sharded_step, H, scores, S, B, d, world, coll_dev, S_job,
+                     stream):
+    """Vocabulary-sharded e2e: per step the host inputs are uploaded from pinned
+    memory, the sharded step runs (NCCL exchanges included) and rank 0 reads
+    the choices back."""
+    import torch
+    n_in = H.shape[0]
+    Hh, sch = H.pin_memory(), scores.pin_memory()
+    Hd = torch.empty(S, B, d, device="cuda")
+    sc = torch.empty(S, B, dtype=torch.float64, device="cuda")
+    fin = torch.zeros(S, B, dtype=torch.uint8, device="cuda")
+    nh = torch.full((S,), B, dtype=torch.int32, device="cuda")
+    ch = torch.zeros(S * B * 24, dtype=torch.uint8, device="cuda")
+    nc = torch.zeros(S, dtype=torch.int32, device="cuda")
+    ch_h = torch.zeros(S * B * 24, dtype=torch.uint8).pin_memory()
+
+    def one(k):
+        with torch.cuda.stream(stream):
+            Hd.copy_(Hh[k % n_in], non_blocking=True)
+            sc.copy_(sch, non_blocking=True)
+            sharded_step(shard, Hd, sc, fin, nh, ch, nc, None)
+            ch_h.copy_(ch, non_blocking=True)
+        stream.synchronize()
+
+    for k in range(args.warmup):
+        one(k)
+    torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        one(k)
+    el = time.perf_counter() - t0
+    t = torch.tensor([el], device=coll_dev)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    el = float(t.item())
+    return {"value": round(S_job * args.steps / el, 1), "unit": UNIT,
+            "h2d_bytes_per_step": S * B * d * 4 + S * B * 8, "d2h_bytes_per_step": S * B * 24,
+            "api": "vocab_shard.sharded_step (C ABI phases + NCCL all-gathers), one host sync "
+                   "per step"}
+
+
+def run_extras(ctx, model, idx, Hd, sc, fin, nh, choices, nchoice, hout, args, lsh_value, c):
+    """Same-GPU comparison legs (rank 0, one GPU): the full-vocabulary fused
+    path, cfg1 latency, the other arithmetic mode and its choice agreement,
+    recall@B at the bench inputs, and the reference's validated operating
+    point (LSH vs full speed-up at matched top-B agreement)."""
+    import numpy as np
     import torch
 
     from paper_1806_00588_b200 import FAST, PARITY, Batch
-    c = CFG
-    S, B, d = c["S"], c["B"], c["d"]
+    from paper_1806_00588_b200.lshbeam import exact_topb
+    S, B, d, V = c["S"], c["B"], c["d"], c["V"]
     out = {}
     base, step_bytes = Hd.data_ptr(), S * B * d * 4
+    timer = dev_timer(ctx)
 
-    def time_batch(b, steps):
-        for k in range(2):
+    def time_batch(b, steps, warm=2):
+        for k in range(warm):
             b.step(base + k * step_bytes, sc, fin, nh, choices, nchoice, hout)
         ctx.sync()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        st = torch.cuda.ExternalStream(ctx.stream)
-        s.record(st)
-        for k in range(steps):
-            b.step(base + (k % c["inputs"]) * step_bytes, sc, fin, nh, choices, nchoice, hout)
-        e.record(st)
-        torch.cuda.synchronize()
-        ctx.sync()
-        return s.elapsed_time(e) / steps
+        return timer(lambda k: b.step(base + (k % c["inputs"]) * step_bytes, sc, fin, nh,
+                                      choices, nchoice, hout), steps)
 
-    for name, mode in [("full_vocab_parity", PARITY), ("full_vocab_fast", FAST)]:
-        b = Batch(ctx, model, None, S=S, B=B, specials=[c["V"] - 1], mode=mode, full_vocab=True)
+    for nm, mode in [("full_vocab_parity", PARITY), ("full_vocab_fast", FAST)]:
+        b = Batch(ctx, model, None, S=S, B=B, specials=[V - 1], mode=mode, full_vocab=True)
         ms = time_batch(b, 5)
-        out[name] = {"ms_per_step": round(ms, 4), "value": round(S / (ms / 1e3), 1),
-                     "lsh_speedup": round(lsh_value / (S / (ms / 1e3)), 2)}
+        out[nm] = {"ms_per_step": round(ms, 4), "value": round(S / (ms / 1e3), 1),
+                   "lsh_speedup": round(lsh_value / (S / (ms / 1e3)), 2)}
         b.close()
     other = FAST if args.mode == "parity" else PARITY
-    b = Batch(ctx, model, idx, S=S, B=B, T=c["T"], t=c["t"], specials=[c["V"] - 1], mode=other)
-    ms = time_batch(b, 50)
+    bo = Batch(ctx, model, idx, S=S, B=B, T=c["T"], t=c["t"], specials=[V - 1], mode=other)
+    ms = time_batch(bo, 50)
     out["lsh_" + ("fast" if other == FAST else "parity")] = {
         "ms_per_step": round(ms, 4), "value": round(S / (ms / 1e3), 1)}
-    # chosen-token agreement of FAST (tensor cores / FFMA) with PARITY on the
-    # same 50 step inputs: (beam, word) of every choice
-    bp = Batch(ctx, model, idx, S=S, B=B, T=c["T"], t=c["t"], specials=[c["V"] - 1], mode=PARITY)
-    bf = b if other == FAST else Batch(ctx, model, idx, S=S, B=B, T=c["T"], t=c["t"],
-                                       specials=[c["V"] - 1], mode=FAST)
+    # chosen (beam, word) agreement of FAST with PARITY on the same 50 inputs
+    bp = Batch(ctx, model, idx, S=S, B=B, T=c["T"], t=c["t"], specials=[V - 1], mode=PARITY)
+    bf = bo if other == FAST else Batch(ctx, model, idx, S=S, B=B, T=c["T"], t=c["t"],
+                                        specials=[V - 1], mode=FAST)
     agree = total = 0
     for k in range(c["inputs"]):
         got = []
@@ -399,14 +515,7 @@ def run_extras(ctx, model, idx, Hd, sc, fin, nh, choices, nchoice, hout, args, l
         total += same.numel()
     out["fast_vs_parity_choice_agreement"] = {"agree": agree, "total": total,
                                               "frac": round(agree / max(total, 1), 6)}
-    # recall@B vs full (SURVEY §8 d): per row, the fraction of the exact
-    # full-vocabulary top-B logits (+bias) that the LSH candidate set holds,
-    # on the first 4 step inputs. The candidate sets are the reference's own
-    # (bit-exact), so this is the reference's recall on the same inputs; for
-    # iid random E and H it is near chance (the paper's recall needs trained
-    # embeddings; the reference's operating point is acceptance criterion 5).
-    from paper_1806_00588_b200.lshbeam import exact_topb
-    import numpy as np
+    # recall@B vs full (SURVEY §8 d) on the first 4 inputs
     hits = rows = 0
     for k in range(4):
         bp.step(base + k * step_bytes, sc, fin, nh, choices, nchoice, hout)
@@ -414,24 +523,196 @@ def run_extras(ctx, model, idx, Hd, sc, fin, nh, choices, nchoice, hout, args, l
         ids_exact, _ = exact_topb(ctx, model, base + k * step_bytes, S * B, B, bias=True)
         for s_ in range(S):
             cand = bp.candidates(s_)[0]
-            ex = ids_exact[s_ * B:(s_ + 1) * B]
-            hits += int(np.isin(ex, cand).sum())
+            hits += int(np.isin(ids_exact[s_ * B:(s_ + 1) * B], cand).sum())
             rows += B
     out["recall_at_B"] = {"value": round(hits / max(rows * B, 1), 4), "rows": rows,
-                          "note": "exact full-vocab top-B vs V_LSH, 4 inputs x 768 rows; "
-                                  "iid synthetic data: near chance, same as the reference"}
-    for bb in {id(bp): bp, id(bf): bf, id(b): b}.values():
+                          "note": "exact full-vocab top-B vs V_LSH, 4 inputs x 768 rows; iid "
+                                  "synthetic data: near chance, the reference's value too "
+                                  "(see operating_point for trained-like data)"}
+    for bb in {id(bp): bp, id(bf): bf, id(bo): bo}.values():
         bb.close()
+    out["cfg1"] = run_cfg1(ctx, model, idx, c)
+    out["operating_point"] = run_operating_point(ctx)
     return out
 
 
+def run_cfg1(ctx, model, idx, c):
+    """BASELINE configs[0]: one sentence (S=1, B=12) per step, |V|=40k, d=1000:
+    latency of the LSH step, eager (five PDL-chained launches) and replayed
+    as one CUDA graph, vs the full-vocabulary step."""
+    import torch
+
+    from paper_1806_00588_b200 import PARITY, Batch
+    B, d, V = c["B"], c["d"], c["V"]
+    g = torch.Generator().manual_seed(3)
+    n_in = 64
+    H = torch.randn(n_in, 1, B, d, generator=g).cuda()
+    sc = (-torch.rand(1, B, generator=g, dtype=torch.float64) * 4).cuda()
+    fin = torch.zeros(1, B, dtype=torch.uint8, device="cuda")
+    nh = torch.full((1,), B, dtype=torch.int32, device="cuda")
+    ch = torch.zeros(B * 24, dtype=torch.uint8, device="cuda")
+    nc = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ho = torch.empty(1, B, d, device="cuda")
+    Hcur = torch.empty(1, B, d, device="cuda")
+    timer = dev_timer(ctx)
+    st = torch.cuda.ExternalStream(ctx.stream)
+    res = {}
+    for nm, full in (("lsh", False), ("full_vocab", True)):
+        b = Batch(ctx, model, None if full else idx, S=1, B=B, T=0 if full else c["T"],
+                  t=0 if full else c["t"], specials=[V - 1], mode=PARITY, full_vocab=full)
+
+        def eager(k, b=b):
+            b.step(H[k % n_in], sc, fin, nh, ch, nc, ho)
+        for k in range(5):
+            eager(k)
+        ctx.sync()
+        ms = timer(eager, 200)
+        r = {"us_per_step": round(ms * 1e3, 2), "steps_per_s": round(1e3 / ms, 1)}
+        # graph: the captured step reads Hcur; each replay's input is copied
+        # in first (the decode loop writes it in place; the copy is timed too)
+        with torch.cuda.stream(st):
+            Hcur.copy_(H[0])
+        b.graph_capture(Hcur, sc, fin, nh, ch, nc, ho)
+
+        def replay(k, b=b):
+            with torch.cuda.stream(st):
+                Hcur.copy_(H[k % n_in], non_blocking=True)
+            b.graph_launch()
+        for k in range(5):
+            replay(k)
+        ctx.sync()
+        msg = timer(replay, 200)
+        r["graph_us_per_step"] = round(msg * 1e3, 2)
+        r["graph_steps_per_s"] = round(1e3 / msg, 1)
+        res[nm] = r
+        b.close()
+    res["lsh_speedup_vs_full"] = round(res["full_vocab"]["us_per_step"] /
+                                       res["lsh"]["us_per_step"], 2)
+    res["note"] = ("device-timed (CUDA events on the step stream), 200 steps over 64 cycled "
+                   "inputs; graph = lsb_batch_graph_capture/launch, includes a 48 KB "
+                   "device copy of the step input")
+    return res
+
+
+def run_operating_point(ctx, S=64, steps=8):
+    """The reference's validated operating point (tests/acceptance.cpp:275-300,
+    BASELINE.md §2b): V=50k, d=256, Zipf bias 300, K=16, u=3, W=500, T=250,
+    t=5, batched over S=64 synthetic decodes (h0_s from mix_seed(7, 100+s),
+    the model provider's W_h / W_e recurrence on the device). Per step both
+    paths score the SAME state: the LSH step's choices drive the decode; the
+    full-vocabulary step's choices on that state are the agreement target.
+    Reports recall@B (exact full top-B inside V_LSH), top-B choice agreement
+    (fraction of the full path's (beam, word) choices the LSH path also
+    chose), and the device time of both paths over the recorded states in
+    each arithmetic mode."""
+    import torch
+
+    from paper_1806_00588_b200.synth import synth_model
+    V, d, bias_s, K, u, W, T, t, B = 50000, 256, 300.0, 16, 3, 500, 250, 5, 12
+    E, bias, wh, we, _ = synth_model(V, d, 7, bias_s)
+    # torch work on the context's stream (ordered with the library's kernels)
+    with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream)):
+        return _operating_point(ctx, S, steps, V, d, K, u, W, T, t, B, E, bias, wh, we)
+
+
+def _operating_point(ctx, S, steps, V, d, K, u, W, T, t, B, E, bias, wh, we):
+    import numpy as np
+    import torch
+
+    from paper_1806_00588_b200 import FAST, PARITY, Batch, Index, Model
+    from paper_1806_00588_b200.lshbeam import Recurrent, exact_topb
+    from paper_1806_00588_b200.seeds import mix_seed
+    from paper_1806_00588_b200.synth import start_state
+    model = Model(ctx, E, bias)
+    idx = Index(ctx, model, K=K, u=u, W=W, perm_seed=mix_seed(7, 1), index_seed=mix_seed(7, 2))
+    rec = Recurrent(ctx, wh, we)
+    dev = torch.device("cuda", ctx.device)
+    mk = lambda full, mode: Batch(ctx, model, None if full else idx, S=S, B=B,  # noqa: E731
+                                  T=0 if full else T, t=0 if full else t, specials=[V - 1],
+                                  mode=mode, full_vocab=full)
+    lsh, full = mk(False, PARITY), mk(True, PARITY)
+    H = torch.zeros(S, B, d, device=dev)
+    H[:, 0] = torch.from_numpy(np.stack([start_state(7, s, d) for s in range(S)])).to(dev)
+    sc = torch.zeros(S, B, dtype=torch.float64, device=dev)
+    fin = torch.zeros(S, B, dtype=torch.uint8, device=dev)
+    nh = torch.ones(S, dtype=torch.int32, device=dev)  # step 0: one live hypothesis
+    chL = torch.zeros(S * B * 24, dtype=torch.uint8, device=dev)
+    chF = torch.zeros_like(chL)
+    ncL = torch.zeros(S, dtype=torch.int32, device=dev)
+    ncF = torch.zeros_like(ncL)
+    ho = torch.empty(S, B, d, device=dev)
+    hoF = torch.empty_like(ho)
+    states = []
+    hits = rows = agree = want = 0
+    vl = []
+    dt = np.dtype([("score", "<f8"), ("beam", "<u4"), ("pad", "<u4"), ("word", "<i8")])
+    for k in range(steps):
+        states.append((H.clone(), sc.clone(), fin.clone(), nh.clone()))
+        lsh.step(H, sc, fin, nh, chL, ncL, ho)
+        full.step(H, sc, fin, nh, chF, ncF, hoF)
+        ctx.sync()
+        cl = np.frombuffer(chL.cpu().numpy().tobytes(), dt).reshape(S, B)
+        cf = np.frombuffer(chF.cpu().numpy().tobytes(), dt).reshape(S, B)
+        nl, nf, nhh, finh = (ncL.cpu().numpy(), ncF.cpu().numpy(), nh.cpu().numpy(),
+                             fin.cpu().numpy())
+        for s in range(S):
+            a = {(int(x["beam"]), int(x["word"])) for x in cl[s, :nl[s]]}
+            f = {(int(x["beam"]), int(x["word"])) for x in cf[s, :nf[s]]}
+            agree += len(a & f)
+            want += len(f)
+            vl.append(len(lsh.candidates(s)[0]))
+        # recall@B over the live rows (exact full-vocabulary top-B + bias)
+        ids_exact, _ = exact_topb(ctx, model, H.data_ptr(), S * B, B, bias=True)
+        for s in range(S):
+            cand = lsh.candidates(s)[0]
+            for i in range(int(nhh[s])):
+                if finh[s, i]:
+                    continue
+                hits += int(np.isin(ids_exact[s * B + i], cand).sum())
+                rows += 1
+        # advance the decode with the LSH choices: parent rows are in ho;
+        # new hidden = recurrence(parent, token); EOS (V-1) freezes
+        words = torch.from_numpy(np.ascontiguousarray(
+            np.where(np.arange(B)[None, :] < nl[:, None], cl["word"], -1))).to(dev)
+        newH = torch.empty_like(H)
+        rec.step(model, ho.data_ptr(), words.data_ptr(), S * B, newH.data_ptr())
+        H = newH
+        sc = torch.from_numpy(np.ascontiguousarray(cl["score"])).to(dev)
+        fin = ((words == V - 1) | (words < 0)).to(torch.uint8)
+        nh = torch.from_numpy(nl.astype(np.int32)).to(dev)
+        ctx.sync()
+    res = {"config": "V=50000 d=256 bias=300 K=16 u=3 W=500 T=250 t=5 B=12, %d synthetic "
+                     "decodes x %d steps (reference acceptance operating point, batched)"
+                     % (S, steps),
+           "recall_at_B": round(hits / max(rows * B, 1), 4),
+           "topB_choice_agreement": round(agree / max(want, 1), 4),
+           "mean_vlsh": round(float(np.mean(vl)), 1)}
+    lsh.close(), full.close()
+    timer = dev_timer(ctx)
+    for mname, mode in (("parity", PARITY), ("fast", FAST)):
+        bl, bf = mk(False, mode), mk(True, mode)
+        tms = {}
+        for nm, b in (("lsh", bl), ("full_vocab", bf)):
+            for st in states[:2]:
+                b.step(*st, chL, ncL, ho)
+            ctx.sync()
+            tms[nm] = timer(lambda k, b=b: b.step(*states[k % len(states)], chL, ncL, ho),
+                            3 * len(states))
+        res[mname] = {"lsh_ms_per_step": round(tms["lsh"], 4),
+                      "full_vocab_ms_per_step": round(tms["full_vocab"], 4),
+                      "lsh_speedup": round(tms["full_vocab"] / tms["lsh"], 2)}
+        bl.close(), bf.close()
+    rec.close(), idx.close(), model.close()
+    return res
+
+
 # ------------------------------------------------------------ reference
-def cpu_baseline(E, bias, H, scores, seconds, steps=None):
+def cpu_baseline(name, E, bias, H, scores, seconds, steps=None):
     """The reference's own CPU step (oracle/_ref) on the host cores, on a
     bounded sample of the same workload."""
     from oracle.oracle import Reference, ReferenceStepper
     from paper_1806_00588_b200.seeds import mix_seed
-    c = CFG
+    c = WORKLOADS[name]
     if not Reference.available():
         return {"value": None, "unit": UNIT, "kind": "reference",
                 "note": "oracle/_ref not built"}
@@ -439,6 +720,7 @@ def cpu_baseline(E, bias, H, scores, seconds, steps=None):
     cores = os.cpu_count() or 1
     ref.set_threads(cores)
     En, bn, Hn, scn = E.numpy(), bias.numpy(), H.numpy(), scores.numpy()
+    S = Hn.shape[1]
     st = ReferenceStepper(ref, En, bn, c["K"], c["u"], c["W"], mix_seed(c["seed"], 1),
                           mix_seed(c["seed"], 2))
     for s in range(2):  # warm-up
@@ -446,7 +728,7 @@ def cpu_baseline(E, bias, H, scores, seconds, steps=None):
     n, t0 = 0, time.perf_counter()
     k = 0
     while True:
-        for s in range(c["S"]):
+        for s in range(S):
             st.step(Hn[k % c["inputs"], s], scn[s], c["B"], c["T"], c["t"], [c["V"] - 1])
             n += 1
         k += 1
@@ -455,7 +737,7 @@ def cpu_baseline(E, bias, H, scores, seconds, steps=None):
             break
     st.close()
     return {"value": round(n / el, 2), "unit": UNIT, "cores": cores, "kind": "reference",
-            "sample": f"{k} batch-steps x {c['S']} sentences = {n} sentence-steps of the same "
+            "sample": f"{k} batch-steps x {S} sentences = {n} sentence-steps of the same "
                       f"workload ({el:.1f} s), reference lshbeam compiled from /root/reference "
                       "sources (g++ -O3 -fopenmp), OMP threads = all host cores"}
 
@@ -463,25 +745,29 @@ def cpu_baseline(E, bias, H, scores, seconds, steps=None):
 def run_reference(args, rank, world, local):
     if rank != 0:
         return
-    c = CFG
-    E, bias, H, scores = make_inputs(0)
+    name = args.workload
+    c = WORKLOADS[name]
+    E, bias, H, scores = make_inputs(name, 0, 1)
     from oracle.oracle import Reference
     if not Reference.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    cb = cpu_baseline(E, bias, H, scores, 0, steps=args.warmup)  # warm-up steps
+    # keep the whole --steps/--warmup run within a few minutes: each "step" is
+    # the cfg2 batch (64 sentences), or a bounded 8-sentence sample of the
+    # heavier cfg3 / cfg4 batches
+    ns = 64 if name == "cfg2" else 8
+    Hs, scs = H[:, :ns], scores[:ns]
+    cpu_baseline(name, E, bias, Hs, scs, 0, steps=args.warmup)  # warm-up steps
     t0 = time.perf_counter()
-    cb = cpu_baseline(E, bias, H, scores, 0, steps=args.steps)
+    cb = cpu_baseline(name, E, bias, Hs, scs, 0, steps=args.steps)
     wall = time.perf_counter() - t0
     v = cb["value"]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(1e3 * c["S"] / v, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (torch.randn seed 7; E 40000x1000 fp32)",
-            "config": {"workload": "cfg2: batched decode step, 64 sentences x B=12, "
-                                   "|V|=40000, d=1000, K=8 u=3 W=16, T=1000, t=2",
-                       "parallelism": "host OpenMP"},
+            "ms_per_step": round(1e3 * c["S"] / v, 3) if v else None, "higher_is_better": True,
+            "scaling": c["scaling"], "vs_baseline": None, "dtype": "f32", "mode": "parity",
+            "data": "synthetic (torch.randn seed 7; E %dx%d fp32)" % (c["V"], c["d"]),
+            "config": workload_config(name, world),
             "cpu_baseline": cb, "wall_s": round(wall, 2),
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

@@ -244,6 +244,11 @@ lsb_status lsb_step_host(lsb_batch* b, const lsb_state_host* in, lsb_choice* cho
 lsb_status lsb_step_host_async(lsb_batch* b, const lsb_state_host* in, lsb_choice* choices_host,
                                int32_t* n_choices_host);
 lsb_status lsb_batch_wait(lsb_batch* b);   /* drain + surface device errors */
+/* lsb_step recorded once as a CUDA graph on these fixed device buffers, then
+ * replayed with one launch per step (the decode loop rewrites the buffers in
+ * place). The context must own a created stream (not the legacy default). */
+lsb_status lsb_batch_graph_capture(lsb_batch* b, const lsb_state_dev* in, const lsb_out_dev* out);
+lsb_status lsb_batch_graph_launch(lsb_batch* b);
 
 /* Per-sentence views of the last step (device -> host copies, synchronous):
  * candidate ids (|V_LSH| of them, ascending), provenance

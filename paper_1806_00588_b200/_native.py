@@ -99,6 +99,8 @@ _SIGS = [
     ("lsb_step_host", C.c_int, [VP, C.POINTER(lsb_state_host), VP, VP, VP]),
     ("lsb_step_host_async", C.c_int, [VP, C.POINTER(lsb_state_host), VP, VP]),
     ("lsb_batch_wait", C.c_int, [VP]),
+    ("lsb_batch_graph_capture", C.c_int, [VP, C.POINTER(lsb_state_dev), C.POINTER(lsb_out_dev)]),
+    ("lsb_batch_graph_launch", C.c_int, [VP]),
     ("lsb_batch_candidates", C.c_int, [VP, C.c_int, VP, C.POINTER(U32), VP]),
     ("lsb_batch_query_codes", C.c_int, [VP, C.c_int, VP]),
     ("lsb_batch_probs", C.c_int, [VP, C.c_int, VP, C.POINTER(C.c_int)]),

@@ -68,6 +68,10 @@ struct lsb_batch {
   cudaStream_t copy_stream = nullptr;   // uploads
   cudaStream_t down_stream = nullptr;   // read-backs
   int next_slot = 0;
+  // CUDA graph of one lsb_step on fixed device buffers (lsb_batch_graph_*)
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  uint64_t graph_kernels = 0;   // kernel launches recorded in the graph
   // last step (for the per-sentence views)
   lsb_state_dev last{};
   bool has_last = false;

@@ -73,6 +73,16 @@ lsb_status lsb_ctx_create(int device, void* stream, lsb_ctx** out) {
   c->device = device;
   c->sm_count = prop.multiProcessorCount;
   c->smem_optin = prop.sharedMemPerBlockOptin;
+  {
+    // stream-ordered scratch (index builds, stage calls): keep up to 512 MB
+    // of freed blocks in the device's default pool instead of unmapping them
+    // at every synchronisation
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = 512ull << 20;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   if (stream) {
     c->stream = static_cast<cudaStream_t>(stream);
   } else {

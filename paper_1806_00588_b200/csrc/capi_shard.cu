@@ -258,6 +258,9 @@ static lsb_status shard_phase3(lsb_batch* b, const lsb_state_dev* in, const doub
                                                    G, R, Bp, b->B, b->B, in->finished, in->n_hyp,
                                                    b->top, b->top_n, ctx->err_dev);
   LSB_LAUNCHED(ctx, "k_shard_combine");
+  // profiled steps: phase 1 recorded stage events 0..3 (step_front); the
+  // softmax stage spans phase 2 + the exchange + the combine
+  if (b->rec) LSB_CUDA(cudaEventRecord(b->ev[4], ctx->stream));
   ExpandArgs ea{};
   ea.S = b->S;
   ea.Bsent = b->B;
@@ -274,7 +277,10 @@ static lsb_status shard_phase3(lsb_batch* b, const lsb_state_dev* in, const doub
   ea.hidden_out = out->hidden_out;
   ea.choices = out->choices;
   ea.n_choices = out->n_choices;
-  return launch_expand(ctx, ea);
+  lsb_status rc = launch_expand(ctx, ea);
+  if (rc) return rc;
+  if (b->rec) LSB_CUDA(cudaEventRecord(b->ev[5], ctx->stream));
+  return LSB_OK;
 }
 
 lsb_status lsb_shard_phase3(lsb_batch* b, const lsb_state_dev* in, const double* allsum_dev,

@@ -40,6 +40,8 @@ lsb_status free_batch(lsb_batch* b) {
     if (sl.consumed) cudaEventDestroy(sl.consumed);
     if (sl.computed) cudaEventDestroy(sl.computed);
   }
+  if (b->graph_exec) cudaGraphExecDestroy(b->graph_exec);
+  if (b->graph) cudaGraphDestroy(b->graph);
   if (b->copy_stream) cudaStreamDestroy(b->copy_stream);
   if (b->down_stream) cudaStreamDestroy(b->down_stream);
   for (auto& e : b->ring)
@@ -550,5 +552,51 @@ lsb_status lsb_batch_probs(lsb_batch* b, int s, float* probs_host, int* n_live) 
 }
 
 const uint32_t* lsb_batch_n_cand_dev(lsb_batch* b) { return b ? b->n_cand : nullptr; }
+
+// One lsb_step recorded as a CUDA graph on the context stream (the PDL
+// launch attributes become programmatic edges), replayed with one
+// cudaGraphLaunch per step: the decode loop updates the same device buffers
+// in place every step, so their addresses are fixed. Replaces the five
+// per-kernel host launches of a small batch by one.
+lsb_status lsb_batch_graph_capture(lsb_batch* b, const lsb_state_dev* in, const lsb_out_dev* out) {
+  if (!b || !in || !out) return set_error("lsb_batch_graph_capture: null argument"), LSB_EINVAL;
+  lsb_ctx* ctx = b->ctx;
+  if (ctx->stream == nullptr || ctx->stream == cudaStreamLegacy || ctx->stream == cudaStreamPerThread)
+    return set_error("lsb_batch_graph_capture: needs a created (non-default) stream"), LSB_EINVAL;
+  if (b->graph_exec) cudaGraphExecDestroy(b->graph_exec);
+  if (b->graph) cudaGraphDestroy(b->graph);
+  b->graph_exec = nullptr;
+  b->graph = nullptr;
+  // one eager step first: kernel attributes (shared-memory limits) and lazily
+  // created side streams are set up outside the capture
+  lsb_status rc = lsb_step(b, in, out);
+  if (rc) return rc;
+  LSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  const bool prof = b->profile;
+  b->profile = false;  // no stage events inside the graph
+  const uint64_t before = ctx->launches;
+  LSB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  rc = lsb_step(b, in, out);
+  cudaGraph_t g = nullptr;
+  const cudaError_t ee = cudaStreamEndCapture(ctx->stream, &g);
+  b->profile = prof;
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  LSB_CUDA(ee);
+  b->graph_kernels = ctx->launches - before;
+  ctx->launches = before;
+  b->graph = g;
+  LSB_CUDA(cudaGraphInstantiate(&b->graph_exec, g, 0));
+  return LSB_OK;
+}
+
+lsb_status lsb_batch_graph_launch(lsb_batch* b) {
+  if (!b || !b->graph_exec) return set_error("lsb_batch_graph_launch: no captured graph"), LSB_EINVAL;
+  LSB_CUDA(cudaGraphLaunch(b->graph_exec, b->ctx->stream));
+  b->ctx->launches += b->graph_kernels;
+  return LSB_OK;
+}
 
 }  // extern "C"

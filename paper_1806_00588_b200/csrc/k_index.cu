@@ -19,6 +19,7 @@
 //     kMaxDisplacements hops and, on failure, retry with the next multiplier
 //     pair of SplitMix64(mix_seed(seed, w)) (src/band_index.cpp:44-70).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -233,15 +234,27 @@ __global__ void __launch_bounds__(1024) k_cuckoo_build(
     const uint32_t* __restrict__ elen, const uint32_t* __restrict__ n_entries, uint32_t V,
     unsigned long long index_seed, BandMeta* __restrict__ bands,
     unsigned long long* __restrict__ tmp, uint4* __restrict__ slots,
-    uint32_t* __restrict__ attempts_out, uint32_t* err, int sequential) {
+    uint32_t* __restrict__ attempts_out, uint32_t* err, int sequential, int smem_cap) {
   __shared__ unsigned long long mul[2];
   __shared__ int fail;
+  extern __shared__ __align__(16) unsigned long long sm_tab[];
   const int w = blockIdx.x;
   const size_t off = static_cast<size_t>(w) * V;
   const uint32_t ne = n_entries[w];
   BandMeta m = bands[w];
   const uint32_t cap = 1u << m.lg;
-  unsigned long long* t = tmp + m.slot_off;
+  // The band's two tables (and its keys) live in shared memory when they fit
+  // (smem_cap >= cap): the reference-order insertion is one thread's serial
+  // eviction chain, so its per-hop latency is the build time (global-memory
+  // atomics: 772 us at cfg 2, shared memory: see DESIGN §4).
+  const bool in_smem = cap <= static_cast<uint32_t>(smem_cap);
+  unsigned long long* t = in_smem ? sm_tab : tmp + m.slot_off;
+  const uint32_t* keys = ekey + off;
+  if (in_smem) {
+    uint32_t* sk = reinterpret_cast<uint32_t*>(sm_tab + 2 * cap);
+    for (uint32_t e = threadIdx.x; e < ne; e += blockDim.x) sk[e] = ekey[off + e];
+    keys = sk;
+  }
   unsigned long long g = mix_seed_dev(index_seed, static_cast<unsigned long long>(w));
   for (int attempt = 0; attempt <= kMaxRebuilds; ++attempt) {
     if (threadIdx.x == 0) {
@@ -255,13 +268,19 @@ __global__ void __launch_bounds__(1024) k_cuckoo_build(
     const uint32_t e0 = sequential ? (threadIdx.x == 0 ? 0u : ne) : threadIdx.x;
     const uint32_t estep = sequential ? 1u : blockDim.x;
     for (uint32_t e = e0; e < ne; e += estep) {
-      unsigned long long cur = (static_cast<unsigned long long>(ekey[off + e]) << 32) | e;
+      unsigned long long cur = (static_cast<unsigned long long>(keys[e]) << 32) | e;
       int table = 0;
       bool placed = false;
       for (int hop = 0; hop < kMaxDisplacements; ++hop) {
         const uint32_t key = static_cast<uint32_t>(cur >> 32);
         const uint32_t pos = table ? cap + slot_of(m1, m.lg, key) : slot_of(m0, m.lg, key);
-        cur = atomicExch(t + pos, cur);
+        if (sequential) {  // one thread: plain swap (shared-memory 64-bit atomics are slow)
+          const unsigned long long prev = t[pos];
+          t[pos] = cur;
+          cur = prev;
+        } else {
+          cur = atomicExch(t + pos, cur);
+        }
         if (cur == kEmpty64) {
           placed = true;
           break;
@@ -401,12 +420,29 @@ lsb_status launch_wta_hash(lsb_ctx* ctx, const float* M, long long n, int d,
 // Device buffer that frees itself.
 template <class T>
 struct DevBuf {
+  // stream-ordered scratch (cudaMallocAsync / cudaFreeAsync on the context
+  // stream): the build's dozen temporaries cost no device-wide allocator
+  // synchronisation (cudaMalloc + cudaFree: ~5 ms of a 6 ms cfg-2 build)
   T* p = nullptr;
+  cudaStream_t st = nullptr;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, st);
   }
-  cudaError_t alloc(size_t n) { return cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)); }
+  cudaError_t alloc(size_t n, cudaStream_t stream) {
+    st = stream;
+    return cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(n, 1) * sizeof(T), st);
+  }
 };
+
+// Largest table capacity (2^lg slots per table) whose two tables (8 B per
+// slot) and keys (4 B per entry, <= 2^lg) fit the device's shared memory;
+// 0 = none (global tables).
+static int cuckoo_smem_cap(const lsb_ctx* ctx, uint32_t lg_max) {
+  static const bool off = getenv("LSB_CUCKOO_GLOBAL") != nullptr;
+  if (off || lg_max > 16) return 0;
+  const size_t need = (static_cast<size_t>(1) << lg_max) * 20;
+  return need + 64 <= ctx->smem_optin ? (1 << lg_max) : 0;
+}
 
 // Builds the band tables of `idx` from device codes (V x W).
 static lsb_status build_bands(lsb_ctx* ctx, lsb_index* idx, const uint32_t* codes_dev,
@@ -415,16 +451,16 @@ static lsb_status build_bands(lsb_ctx* ctx, lsb_index* idx, const uint32_t* code
   const int W = idx->W;
   const size_t VW = static_cast<size_t>(V) * W;
   DevBuf<uint32_t> ka, ia, kb, ib, ekey, estart, elen, nent, maxspan, attempts;
-  LSB_CUDA(ka.alloc(VW));
-  LSB_CUDA(ia.alloc(VW));
-  LSB_CUDA(kb.alloc(VW));
-  LSB_CUDA(ib.alloc(VW));
-  LSB_CUDA(ekey.alloc(VW));
-  LSB_CUDA(estart.alloc(VW));
-  LSB_CUDA(elen.alloc(VW));
-  LSB_CUDA(nent.alloc(W));
-  LSB_CUDA(maxspan.alloc(1));
-  LSB_CUDA(attempts.alloc(1));
+  LSB_CUDA(ka.alloc(VW, ctx->stream));
+  LSB_CUDA(ia.alloc(VW, ctx->stream));
+  LSB_CUDA(kb.alloc(VW, ctx->stream));
+  LSB_CUDA(ib.alloc(VW, ctx->stream));
+  LSB_CUDA(ekey.alloc(VW, ctx->stream));
+  LSB_CUDA(estart.alloc(VW, ctx->stream));
+  LSB_CUDA(elen.alloc(VW, ctx->stream));
+  LSB_CUDA(nent.alloc(W, ctx->stream));
+  LSB_CUDA(maxspan.alloc(1, ctx->stream));
+  LSB_CUDA(attempts.alloc(1, ctx->stream));
   LSB_CUDA(cudaMalloc(&idx->word_ids, std::max<size_t>(VW, 1) * sizeof(uint32_t)));
   LSB_CUDA(cudaMemsetAsync(maxspan.p, 0, 4, ctx->stream));
   LSB_CUDA(cudaMemsetAsync(attempts.p, 0, 4, ctx->stream));
@@ -451,15 +487,21 @@ static lsb_status build_bands(lsb_ctx* ctx, lsb_index* idx, const uint32_t* code
   }
   idx->total_slots = total;
   DevBuf<unsigned long long> tmp;
-  LSB_CUDA(tmp.alloc(total));
+  LSB_CUDA(tmp.alloc(total, ctx->stream));
   LSB_CUDA(cudaMalloc(&idx->slots, std::max<size_t>(total, 1) * sizeof(uint4)));
   LSB_CUDA(cudaMalloc(&idx->bands, W * sizeof(BandMeta)));
   LSB_CUDA(cudaMemcpyAsync(idx->bands, idx->bands_host.data(), W * sizeof(BandMeta),
                            cudaMemcpyHostToDevice, ctx->stream));
-  k_cuckoo_build<<<W, 1024, 0, ctx->stream>>>(ekey.p, estart.p, elen.p, nent.p, V,
-                                              idx->index_seed, idx->bands, tmp.p, idx->slots,
-                                              attempts.p, ctx->err_dev,
-                                              ctx->cuckoo_parallel ? 0 : 1);
+  uint32_t lg_max = 1;
+  for (int w = 0; w < W; ++w) lg_max = std::max(lg_max, idx->bands_host[w].lg);
+  const int smem_cap = cuckoo_smem_cap(ctx, lg_max);
+  const size_t csmem = smem_cap ? static_cast<size_t>(smem_cap) * 20 : 0;
+  if (csmem) LSB_CUDA(cudaFuncSetAttribute(k_cuckoo_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(csmem)));
+  k_cuckoo_build<<<W, 1024, csmem, ctx->stream>>>(ekey.p, estart.p, elen.p, nent.p, V,
+                                                  idx->index_seed, idx->bands, tmp.p, idx->slots,
+                                                  attempts.p, ctx->err_dev,
+                                                  ctx->cuckoo_parallel ? 0 : 1, smem_cap);
   LSB_LAUNCHED(ctx, "k_cuckoo_build");
   LSB_CUDA(cudaMemcpyAsync(idx->bands_host.data(), idx->bands, W * sizeof(BandMeta),
                            cudaMemcpyDeviceToHost, ctx->stream));
@@ -473,15 +515,19 @@ lsb_status build_cuckoo_band(lsb_ctx* ctx, const uint32_t* keys, const uint32_t*
                              uint4* slots_dev, BandMeta* meta_dev, uint32_t* attempts_dev) {
   DevBuf<unsigned long long> tmp;
   DevBuf<uint32_t> ne;
-  LSB_CUDA(tmp.alloc(2u << lg));
-  LSB_CUDA(ne.alloc(1));
+  LSB_CUDA(tmp.alloc(2u << lg, ctx->stream));
+  LSB_CUDA(ne.alloc(1, ctx->stream));
   const BandMeta m{1ull, 1ull, lg, 0};
   LSB_CUDA(cudaMemcpyAsync(ne.p, &n, 4, cudaMemcpyHostToDevice, ctx->stream));
   LSB_CUDA(cudaMemcpyAsync(meta_dev, &m, sizeof(m), cudaMemcpyHostToDevice, ctx->stream));
   LSB_CUDA(cudaMemsetAsync(attempts_dev, 0, 4, ctx->stream));
-  k_cuckoo_build<<<1, 1024, 0, ctx->stream>>>(keys, starts, lens, ne.p, n, seed, meta_dev, tmp.p,
-                                             slots_dev, attempts_dev, ctx->err_dev,
-                                             ctx->cuckoo_parallel ? 0 : 1);
+  const int smem_cap = cuckoo_smem_cap(ctx, lg);
+  const size_t csmem = smem_cap ? static_cast<size_t>(smem_cap) * 20 : 0;
+  if (csmem) LSB_CUDA(cudaFuncSetAttribute(k_cuckoo_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(csmem)));
+  k_cuckoo_build<<<1, 1024, csmem, ctx->stream>>>(keys, starts, lens, ne.p, n, seed, meta_dev, tmp.p,
+                                                 slots_dev, attempts_dev, ctx->err_dev,
+                                                 ctx->cuckoo_parallel ? 0 : 1, smem_cap);
   LSB_LAUNCHED(ctx, "k_cuckoo_build");
   return lsb_ctx_sync(ctx);
 }
@@ -536,7 +582,7 @@ lsb_status lsb_index_build(lsb_ctx* ctx, const lsb_model* model, int K, int u, i
                       cudaMemcpyHostToDevice, ctx->stream);
   if (e != cudaSuccess) return fail(cuda_status(e, "upload perms"));
   DevBuf<uint32_t> codes;
-  e = codes.alloc(static_cast<size_t>(model->V) * W);
+  e = codes.alloc(static_cast<size_t>(model->V) * W, ctx->stream);
   if (e != cudaSuccess) return fail(cuda_status(e, "cudaMalloc codes"));
   st = launch_wta_hash(ctx, model->E, model->V, model->d, idx->perms, K, u, W, codes.p);
   if (st) return fail(st);
@@ -567,7 +613,7 @@ lsb_status lsb_index_build_codes(lsb_ctx* ctx, const uint32_t* codes_host, uint3
   int nbits = 0;
   while (nbits < 32 && (maxc >> nbits)) ++nbits;
   DevBuf<uint32_t> codes;
-  cudaError_t e = codes.alloc(VW);
+  cudaError_t e = codes.alloc(VW, ctx->stream);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(codes.p, codes_host, VW * 4, cudaMemcpyHostToDevice, ctx->stream);
   if (e != cudaSuccess) {
@@ -644,11 +690,11 @@ lsb_status lsb_index_find(lsb_ctx* ctx, const lsb_index* idx, const int32_t* ban
   DevBuf<int32_t> b;
   DevBuf<uint32_t> k, s, l;
   DevBuf<uint8_t> f;
-  LSB_CUDA(b.alloc(n));
-  LSB_CUDA(k.alloc(n));
-  LSB_CUDA(s.alloc(n));
-  LSB_CUDA(l.alloc(n));
-  LSB_CUDA(f.alloc(n));
+  LSB_CUDA(b.alloc(n, ctx->stream));
+  LSB_CUDA(k.alloc(n, ctx->stream));
+  LSB_CUDA(s.alloc(n, ctx->stream));
+  LSB_CUDA(l.alloc(n, ctx->stream));
+  LSB_CUDA(f.alloc(n, ctx->stream));
   LSB_CUDA(cudaMemcpyAsync(b.p, bands_host, n * 4, cudaMemcpyHostToDevice, ctx->stream));
   LSB_CUDA(cudaMemcpyAsync(k.p, keys_host, n * 4, cudaMemcpyHostToDevice, ctx->stream));
   const int wpb = 8;
@@ -674,9 +720,9 @@ lsb_status lsb_wta_hash(lsb_ctx* ctx, const float* M_host, int64_t n, int d,
   if (n == 0) return LSB_OK;
   DevBuf<float> M;
   DevBuf<uint32_t> p, out;
-  LSB_CUDA(M.alloc(static_cast<size_t>(n) * d));
-  LSB_CUDA(p.alloc(P * K));
-  LSB_CUDA(out.alloc(static_cast<size_t>(n) * W));
+  LSB_CUDA(M.alloc(static_cast<size_t>(n) * d, ctx->stream));
+  LSB_CUDA(p.alloc(P * K, ctx->stream));
+  LSB_CUDA(out.alloc(static_cast<size_t>(n) * W, ctx->stream));
   LSB_CUDA(cudaMemcpyAsync(M.p, M_host, static_cast<size_t>(n) * d * 4, cudaMemcpyHostToDevice,
                            ctx->stream));
   LSB_CUDA(cudaMemcpyAsync(p.p, perms_host, P * K * 4, cudaMemcpyHostToDevice, ctx->stream));
@@ -697,8 +743,8 @@ lsb_status lsb_lookup_hits(lsb_ctx* ctx, const lsb_index* idx, const uint32_t* q
   const size_t BV = static_cast<size_t>(B) * idx->V;
   DevBuf<uint32_t> q;
   DevBuf<int32_t> L;
-  LSB_CUDA(q.alloc(static_cast<size_t>(B) * idx->W));
-  LSB_CUDA(L.alloc(BV));
+  LSB_CUDA(q.alloc(static_cast<size_t>(B) * idx->W, ctx->stream));
+  LSB_CUDA(L.alloc(BV, ctx->stream));
   LSB_CUDA(cudaMemcpyAsync(q.p, q_host, static_cast<size_t>(B) * idx->W * 4,
                            cudaMemcpyHostToDevice, ctx->stream));
   LSB_CUDA(cudaMemsetAsync(L.p, 0, BV * 4, ctx->stream));

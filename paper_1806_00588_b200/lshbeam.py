@@ -421,6 +421,19 @@ class Batch:
         out = N.lsb_out_dev(ptr(choices), ptr(n_choices), ptr(hidden_out))
         N.check(self.lib.lsb_step(self.h, C.byref(st), C.byref(out)), "lsb_step")
 
+    def graph_capture(self, hidden, scores, finished=None, n_hyp=None, choices=None,
+                      n_choices=None, hidden_out=None):
+        """Record one device step on these fixed buffers as a CUDA graph
+        (lsb_batch_graph_capture); graph_launch() replays it."""
+        ptr = lambda x: (x if isinstance(x, int) else x.data_ptr()) if x is not None else None
+        st = N.lsb_state_dev(ptr(hidden), ptr(scores), ptr(finished), ptr(n_hyp))
+        out = N.lsb_out_dev(ptr(choices), ptr(n_choices), ptr(hidden_out))
+        N.check(self.lib.lsb_batch_graph_capture(self.h, C.byref(st), C.byref(out)),
+                "lsb_batch_graph_capture")
+
+    def graph_launch(self):
+        N.check(self.lib.lsb_batch_graph_launch(self.h), "lsb_batch_graph_launch")
+
     def step_host(self, hidden, scores, finished=None, n_hyp=None, want_hidden=False):
         """End-to-end step from host arrays; returns (choices list per sentence, hidden_out)."""
         S, B, d = self.S, self.B, self.dim

@@ -292,3 +292,53 @@ def test_fast_step_tensor_cores(ctx, oracle, full):
         total += len(ws)
         np.testing.assert_allclose(np.array([c[0] for c in res[s]]), ws, rtol=0, atol=1e-3)
     assert agree >= 0.99 * total, (agree, total)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_graph_replay_equals_step(oracle, mode):
+    """lsb_batch_graph_capture / _launch: a replayed step on the captured
+    buffers gives the eager step's choices, candidates and hidden reorder,
+    also after the buffers are rewritten in place (the decode-loop pattern)."""
+    import torch
+
+    from paper_1806_00588_b200 import Batch, Context, Index, Model
+    s = torch.cuda.Stream()
+    ctx = Context(0, s.cuda_stream)
+    V, d, K, u, W, S, B, T, t = 6000, 64, 8, 3, 16, 3, 12, 200, 2
+    E, bias, perms, bt, ps, isd = make_world(oracle, V, d, K, u, W, seed=21, bias_strength=4.0)
+    m = Model(ctx, E, bias)
+    idx = Index(ctx, m, K=K, u=u, W=W, perm_seed=ps, index_seed=isd)
+    b = Batch(ctx, m, idx, S=S, B=B, T=T, t=t, specials=[V - 1], mode=mode)
+    dev = torch.device("cuda", 0)
+    states = [make_state(oracle, S, B, d, seed=k, frozen_every=3 if k else 0) for k in range(3)]
+    H = torch.zeros(S, B, d, device=dev)
+    sc = torch.zeros(S, B, dtype=torch.float64, device=dev)
+    fin = torch.zeros(S, B, dtype=torch.uint8, device=dev)
+    nh = torch.zeros(S, dtype=torch.int32, device=dev)
+    ch = torch.zeros(S * B * 24, dtype=torch.uint8, device=dev)
+    nc = torch.zeros(S, dtype=torch.int32, device=dev)
+    ho = torch.zeros(S, B, d, device=dev)
+
+    def load(st):
+        hidden, scores, finished, n_hyp = st
+        with torch.cuda.stream(s):
+            H.copy_(torch.from_numpy(hidden))
+            sc.copy_(torch.from_numpy(scores))
+            fin.copy_(torch.from_numpy(finished))
+            nh.copy_(torch.from_numpy(n_hyp))
+        s.synchronize()
+
+    load(states[0])
+    b.graph_capture(H, sc, fin, nh, ch, nc, ho)
+    for st in states:
+        load(st)
+        with torch.cuda.stream(s):
+            b.step(H, sc, fin, nh, ch, nc, ho)
+        ctx.sync()
+        want = (ch.clone(), nc.clone(), ho.clone())
+        ch.zero_(), nc.zero_(), ho.zero_()
+        torch.cuda.synchronize()
+        b.graph_launch()
+        ctx.sync()
+        assert torch.equal(ch, want[0]) and torch.equal(nc, want[1]) and torch.equal(ho, want[2])
+    b.close(), idx.close(), m.close(), ctx.close()
