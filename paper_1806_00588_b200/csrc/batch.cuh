@@ -36,6 +36,11 @@ struct lsb_batch {
   float* tc_A = nullptr;        // FAST: pre-tiled E[0, n_shared) for tcgen05
   float* tc_H = nullptr;        // FAST: per-step tiled H
   int tc_N = 0;
+  // few rows: band-split K1+K2 (probe_G > 0) with 16-bit hit counters
+  int probe_G = 0;
+  uint32_t* split_cnt = nullptr;     // [S*B][split_words], self-cleaning
+  uint32_t split_words = 0;
+  uint32_t* split_arrive = nullptr;  // [S*B]
   // long rows (full vocabulary / t = 0): segmented K5a scratch
   int seg_P = 0;
   float* seg_max = nullptr;

@@ -29,7 +29,8 @@ lsb_status free_batch(lsb_batch* b) {
                   b->prov,     b->logits,   b->top,        b->top_n,        b->h_hidden,
                   b->h_scores, b->h_finished, b->h_nhyp,   b->h_choices,    b->h_nchoices,
                   b->h_hidden_out, b->sh_top, b->sh_topn, b->tc_A, b->tc_H, b->arrive,
-                  b->seg_max, b->seg_sum, b->seg_top, b->seg_n, b->seg_count};
+                  b->seg_max, b->seg_sum, b->seg_top, b->seg_n, b->seg_count,
+                  b->split_cnt, b->split_arrive};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& sl : b->slot) {
@@ -81,7 +82,10 @@ lsb_status lsb::step_front(lsb_batch* b, const lsb_state_dev* in, int empty_is_e
     pa.bitmap = b->bitmap;
     pa.nwords = b->nwords;
     pa.err = ctx->err_dev;
-    if ((rc = launch_probe(ctx, pa))) return rc;
+    if ((rc = b->probe_G > 0 ? launch_probe_split(ctx, pa, b->probe_G, b->split_cnt,
+                                                  b->split_words, b->split_arrive)
+                             : launch_probe(ctx, pa)))
+      return rc;
   }
   if (b->rec) LSB_CUDA(cudaEventRecord(b->ev[1], st));
   // K3
@@ -204,6 +208,32 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
   if (e == cudaSuccess) e = dalloc(&b->top_n, SB);
   if (e == cudaSuccess) e = dalloc(&b->arrive, b->S);
   if (e == cudaSuccess) e = cudaMemset(b->arrive, 0, b->S * sizeof(uint32_t));
+  // Few rows with many bands (a one-sentence decode at W > 64): k_probe_count
+  // would run S*B CTAs on a 148-SM GPU, each walking every band's span; split
+  // each row's bands over G CTAs (k_probe_split) so the grid covers ~2 CTAs
+  // per SM. Measured at S=1, V=50k, W=500: K=8 (98-word spans) 100 -> 29 us,
+  // K=16 (12-word spans) 35 -> 33 us; at W=16 (cfg 1) it was slower (16.7 vs
+  // 10.8 us: global-counter atomics vs shared-memory ones), so W <= 64 keeps
+  // k_probe_count. LSB_PROBE_SPLIT=0 turns it off, =G forces G.
+  if (e == cudaSuccess && b->idx && b->t > 0) {
+    static const int split_env = getenv("LSB_PROBE_SPLIT") ? atoi(getenv("LSB_PROBE_SPLIT")) : -1;
+    const uint32_t nslices = b->slice_len ? (V + b->slice_len - 1) / b->slice_len : 1;
+    const int R = static_cast<int>(SB);
+    int G = 0;
+    if (split_env > 0) G = split_env;
+    else if (split_env < 0 && b->idx->W > 64 && static_cast<long>(R) * nslices < ctx->sm_count)
+      G = (2 * ctx->sm_count + R - 1) / R;
+    G = std::min(G, b->idx->W);
+    const uint32_t words = ((V + 1) / 2 + 3) & ~3u;
+    if (G > 1 && SB * words * 4 <= (64ull << 20)) {
+      b->probe_G = G;
+      b->split_words = words;
+      e = dalloc(&b->split_cnt, SB * words);
+      if (e == cudaSuccess) e = cudaMemset(b->split_cnt, 0, SB * words * 4);
+      if (e == cudaSuccess) e = dalloc(&b->split_arrive, SB);
+      if (e == cudaSuccess) e = cudaMemset(b->split_arrive, 0, SB * 4);
+    }
+  }
   // every row scores all V words (full vocabulary, t = 0): rows that long
   // take the segmented K5a (one CTA per row segment)
   static const bool seg_off = getenv("LSB_NO_SEG") != nullptr;

@@ -322,6 +322,168 @@ lsb_status launch_probe(lsb_ctx* ctx, const ProbeArgs& a) {
   return LSB_OK;
 }
 
+// ================================================= K1+K2, band-split variant
+// For steps with few hypothesis rows (a one-sentence decode: 12 rows, so
+// k_probe_count would run 12 CTAs on 148 SMs) the row's bands are split
+// over G CTAs: CTA (row, g) hashes and probes bands [W g / G, W (g+1) / G)
+// and walks their spans one warp per band, coalesced, U id loads in flight.
+// Hit counts per (row, word) are 16-bit counters in global memory (L2); the
+// visit that lifts a count to t sets the word's bit in the sentence bitmap
+// (atomicAdd returns the old count, so exactly once). The row's last CTA to
+// finish (arrival counter) zeroes its counters and the counter for the next
+// step -- self-cleaning, so the kernel also replays inside a CUDA graph.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_probe_split(ProbeArgs a, int G, uint32_t* cnt,
+                                                    uint32_t cnt_words, uint32_t* arrive) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const IndexView& ix = a.ix;
+  const int row = blockIdx.x, g = blockIdx.y;
+  const int s = row / a.B, i = row % a.B;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int nwarp = NT / 32;
+  const int w0 = static_cast<int>((static_cast<long long>(ix.W) * g) / G);
+  const int w1 = static_cast<int>((static_cast<long long>(ix.W) * (g + 1)) / G);
+  const int nb = w1 - w0;
+  const int np = nb * ix.u;  // permutations of these bands
+  float* h = reinterpret_cast<float*>(smem);
+  const int dpad = (ix.d + 3) & ~3;
+  uint32_t* sp_start = reinterpret_cast<uint32_t*>(h + dpad);
+  uint32_t* sp_len = sp_start + nb;
+  uint16_t* idx = reinterpret_cast<uint16_t*>(sp_len + nb);
+  constexpr int kMaxKReg = 16;
+  uint32_t pk[kMaxKReg];
+  const int p_own = threadIdx.x;
+  const bool kreg = ix.K <= kMaxKReg;
+  if (p_own < np && kreg) {
+    const uint32_t* pr = ix.perms + static_cast<size_t>(w0 * ix.u + p_own) * ix.K;
+#pragma unroll
+    for (int k = 0; k < kMaxKReg; ++k) pk[k] = k < ix.K ? __ldg(pr + k) : 0u;
+  }
+  pdl_wait();
+  const bool dead = (a.n_hyp && i >= a.n_hyp[s]) || (a.finished && a.finished[row]);
+  if (dead) return;  // uniform over the row's CTAs: no counting, nothing to clear
+  const float* src = a.hidden + static_cast<size_t>(row) * ix.d;
+  int nan = 0;
+  if ((ix.d & 3) == 0) {
+    for (int c = threadIdx.x; c < (ix.d >> 2); c += NT) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(src) + c);
+      nan |= isnan(v.x) | isnan(v.y) | isnan(v.z) | isnan(v.w);
+      reinterpret_cast<float4*>(h)[c] = v;
+    }
+  } else {
+    for (int c = threadIdx.x; c < ix.d; c += NT) {
+      const float v = __ldg(src + c);
+      nan |= isnan(v);
+      h[c] = v;
+    }
+  }
+  if (__syncthreads_or(nan)) {
+    if (threadIdx.x == 0 && g == 0) atomicOr(a.err, kErrNaN);
+    return;  // uniform over the row's CTAs (same row)
+  }
+  // K1 for this CTA's permutations (ties to the smallest k)
+  for (int p = threadIdx.x; p < np; p += NT) {
+    const uint32_t* pr = ix.perms + static_cast<size_t>(w0 * ix.u + p) * ix.K;
+    uint32_t best = 0;
+    if (kreg && p == p_own) {
+      float bv = h[pk[0]];
+#pragma unroll
+      for (int k = 1; k < kMaxKReg; ++k)
+        if (k < ix.K) {
+          const float v = h[pk[k]];
+          if (v > bv) {
+            bv = v;
+            best = k;
+          }
+        }
+    } else {
+      float bv = h[__ldg(pr)];
+      for (int k = 1; k < ix.K; ++k) {
+        const float v = h[__ldg(pr + k)];
+        if (v > bv) {
+          bv = v;
+          best = k;
+        }
+      }
+    }
+    idx[p] = static_cast<uint16_t>(best);
+  }
+  __syncthreads();
+  // codes + cuckoo probe, a thread per band
+  for (int j = threadIdx.x; j < nb; j += NT) {
+    const int w = w0 + j;
+    uint32_t code = 0;
+    for (int b = 0; b < ix.u; ++b) code |= static_cast<uint32_t>(idx[j * ix.u + b]) << (b * ix.bits);
+    a.qcodes[static_cast<size_t>(row) * ix.W + w] = code;
+    const BandMeta m = ix.bands[w];
+    const uint32_t cap = 1u << m.lg;
+    const uint4 s0 = __ldg(ix.slots + m.slot_off + slot_of(m.mul0, m.lg, code));
+    const uint4 s1 = __ldg(ix.slots + m.slot_off + cap + slot_of(m.mul1, m.lg, code));
+    uint32_t st = 0, ln = 0;
+    if (s0.x == code) {  // table 0 wins (the reference probes it first)
+      st = s0.y;
+      ln = s0.z;
+    } else if (s1.x == code) {
+      st = s1.y;
+      ln = s1.z;
+    }
+    sp_start[j] = st;
+    sp_len[j] = ln;
+  }
+  __syncthreads();
+  if (a.t > 0) {
+    uint32_t* bm = a.bitmap + static_cast<size_t>(s) * a.nwords;
+    uint32_t* rc = cnt + static_cast<size_t>(row) * cnt_words;
+    const uint32_t t = static_cast<uint32_t>(a.t);
+    constexpr int U = 4;
+    for (int j = warp; j < nb; j += nwarp) {
+      const uint32_t st = sp_start[j], ln = sp_len[j];
+      const uint32_t* ids = ix.word_ids + static_cast<size_t>(w0 + j) * ix.V + st;
+      for (uint32_t k0 = lane; k0 < ln; k0 += 32 * U) {
+        uint32_t idu[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) idu[u] = k0 + 32 * u < ln ? __ldg(ids + k0 + 32 * u) : 0xFFFFFFFFu;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t id = idu[u];
+          if (id == 0xFFFFFFFFu) continue;
+          const uint32_t sh = (id & 1) * 16;
+          const uint32_t c = (atomicAdd(rc + (id >> 1), 1u << sh) >> sh) & 0xFFFFu;
+          if (c + 1 == t) atomicOr(bm + (id >> 5), 1u << (id & 31));
+        }
+      }
+    }
+  }
+  pdl_trigger();
+  if (a.t <= 0) return;
+  // the row's last CTA clears its counters for the next step
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(arrive + row, 1u) == static_cast<uint32_t>(G - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  uint4* rc4 = reinterpret_cast<uint4*>(cnt + static_cast<size_t>(row) * cnt_words);
+  for (uint32_t k = threadIdx.x; k < cnt_words / 4; k += NT) rc4[k] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) arrive[row] = 0;
+}
+
+lsb_status launch_probe_split(lsb_ctx* ctx, const ProbeArgs& a, int G, uint32_t* cnt,
+                              uint32_t cnt_words, uint32_t* arrive) {
+  const IndexView& ix = a.ix;
+  const int nbmax = (ix.W + G - 1) / G;
+  constexpr int NT = 256;
+  if (nbmax * ix.u > NT * 8) return set_error("probe_split: too many bands per CTA"), LSB_EINVAL;
+  const size_t smem = ((ix.d + 3) & ~3) * 4 + 2 * nbmax * 4 + 2 * nbmax * ix.u + 16;
+  if (smem > ctx->smem_optin) return set_error("probe_split: shared memory budget"), LSB_EINVAL;
+  auto* kern = k_probe_split<NT>;
+  if (lsb_status rc = ensure_smem(ctx, kern, smem)) return rc;
+  LSB_CUDA(launch_pdl(ctx, kern, dim3(a.S * a.B, G), dim3(NT), smem, a, G, cnt, cnt_words, arrive));
+  LSB_LAUNCHED(ctx, "k_probe_split");
+  return LSB_OK;
+}
+
 // ====================================================================== K3
 __device__ __forceinline__ uint32_t below_mask(uint32_t word, uint32_t T) {
   // bits of ids < T inside bitmap word `word`

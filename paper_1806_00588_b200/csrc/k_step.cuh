@@ -109,6 +109,11 @@ struct ExpandArgs {
 };
 
 lsb_status launch_probe(lsb_ctx* ctx, const ProbeArgs& a);
+// Band-split K1+K2 for few rows (k_step.cu): grid (rows, G band groups),
+// 16-bit hit counters cnt[rows][cnt_words] in global memory, zero on entry
+// and left zero (self-cleaning), arrive[rows] zero likewise.
+lsb_status launch_probe_split(lsb_ctx* ctx, const ProbeArgs& a, int G, uint32_t* cnt,
+                              uint32_t cnt_words, uint32_t* arrive);
 lsb_status launch_compact(lsb_ctx* ctx, const CompactArgs& a, int S);
 lsb_status launch_logits(lsb_ctx* ctx, LogitsArgs a, lsb_mode mode, int target_ctas);
 // PARITY one-lane-per-thread kernel (k_logits_ln.cu): applicability and launch.

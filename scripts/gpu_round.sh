@@ -4,7 +4,7 @@
 # usage: scripts/gpu_round.sh [tag] [kernel-regex ...]
 TAG=${1:-r01}
 shift || true
-KERNELS=${*:-k_logits k_probe_count}
+KERNELS=${*:-k_logits k_probe_count k_compact k_softmax_topb k_expand}
 OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > "$OUT/gpu.txt" 2>&1
@@ -29,4 +29,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'^k_' -c 200 --csv \
   --log-file "$OUT/launches_fast.csv" python bench.py --steps 20 --warmup 3 --no-cpu-baseline \
   --no-extras --mode fast > "$OUT/ncu_launch_bench_fast.log" 2>&1
+# the full-vocabulary path (the >= 4x denominator) at S=64: lane-kernel
+# logits and the segmented softmax
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_logits_ln|^k_seg_" -s 4 -c 4 \
+  -f -o "$OUT/prof_full_vocab" python scripts/full_probe.py 64 12 parity 2 > "$OUT/ncu_full_vocab.log" 2>&1
 echo done > "$OUT/DONE"

@@ -104,7 +104,7 @@ def main():
                          f"{100 * sum(v) / tot:.1f}% |")
         open(os.path.join(PROF, f"{tag}_{out_name}.md"), "w").write("\n".join(lines) + "\n")
     summ_path = os.path.join(PROF, "ncu_summary.json")
-    summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
+    summ = {}  # this capture only: no entries from older builds
     md = [f"# {tag}: `ncu --set full` captures", ""]
     for rep in sorted(glob.glob(os.path.join(src, "prof_*.ncu-rep"))):
         for name, m in full_metrics(rep).items():

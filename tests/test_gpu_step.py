@@ -157,6 +157,21 @@ def test_step_parity_under_lane_kernel():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
+def test_step_parity_unsplit_probe():
+    """The same step tests with the band-split probe off (LSB_PROBE_SPLIT=0:
+    k_probe_count for every row count), so both K1+K2 kernels stay covered."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_step.py"), "-k",
+                        "test_step_matches_oracle or test_graph_replay"],
+                       env={**os.environ, "LSB_PROBE_SPLIT": "0"}, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 def test_step_nan_hidden_rejected(ctx, oracle):
     V, d, K, u, W, S, B = 500, 16, 4, 2, 8, 1, 2
     E, bias, perms, bt, ps, isd = make_world(oracle, V, d, K, u, W)
