@@ -58,7 +58,7 @@ GatheredEmbeddings gather_embeddings(const MatF& E, const CandidateSet& cands) {
   for (uint32_t id : cands.word_ids)
     if (id >= E.rows()) throw std::invalid_argument("gather_embeddings: id out of range");
   Guard lock(detail::api_mutex());
-  auto model = detail::upload_model(E.data(), static_cast<uint32_t>(E.rows()),
+  auto model = detail::cached_model(E.data(), static_cast<uint32_t>(E.rows()),
                                     static_cast<int>(E.cols()), nullptr);
   check(lsb_gather_embeddings(detail::ctx(), model.get(), cands.word_ids.data(), n, g.rows.data()),
         "gather_embeddings");

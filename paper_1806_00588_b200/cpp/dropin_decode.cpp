@@ -131,11 +131,10 @@ DecodeResult decode(const SynthModel& model, const DecodeConfig& config, DecodeM
   lsb_ctx* c = detail::ctx();
   const int d = model.dim, B = config.beam;
   const uint32_t V = model.vocab;
-  auto dm = detail::upload_model(model.embeddings.data(), V, d, model.freq_bias.data());
-  lsb_recurrent* rec_raw = nullptr;
-  check(lsb_recurrent_create(c, model.w_hidden.data(), model.w_embed.data(), d, &rec_raw),
-        "decode: recurrence");
-  detail::RecurrentPtr rec(rec_raw);
+  // device copies cached across decode() calls on the same model (the
+  // acceptance grid decodes one model 32 times)
+  auto dm = detail::cached_model(model.embeddings.data(), V, d, model.freq_bias.data());
+  auto rec = detail::cached_recurrent(model.w_hidden.data(), model.w_embed.data(), d);
   lsb_index* ix = mode == DecodeMode::kLsh
                       ? lsh->bands.device_with_perms(lsh->perms, lsh->params.u)
                       : nullptr;

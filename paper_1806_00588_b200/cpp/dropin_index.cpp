@@ -221,7 +221,7 @@ LshIndex build_lsh_index(const MatF& embeddings, const WtaParams& params, uint64
   const int d = static_cast<int>(embeddings.cols());
   PermutationSet perms = generate_permutations(d, params);  // validates d >= K
   Guard g(detail::api_mutex());
-  auto model = detail::upload_model(embeddings.data(), static_cast<uint32_t>(embeddings.rows()),
+  auto model = detail::cached_model(embeddings.data(), static_cast<uint32_t>(embeddings.rows()),
                                     d, nullptr);
   lsb_index* idx = nullptr;
   const lsb_status st = lsb_index_build(detail::ctx(), model.get(), params.K, params.u, params.W,

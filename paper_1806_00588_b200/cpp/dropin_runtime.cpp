@@ -1,7 +1,9 @@
 // dropin_runtime.cpp -- see dropin_runtime.hpp.
 #include "dropin_runtime.hpp"
 
+#include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 namespace lshbeam::detail {
 
@@ -56,6 +58,85 @@ ModelPtr upload_model(const float* E, uint32_t vocab, int dim, const float* bias
   lsb_model* m = nullptr;
   check(lsb_model_create(ctx(), E, vocab, dim, bias, &m), "model upload");
   return ModelPtr(m);
+}
+
+namespace {
+
+uint64_t mix64(uint64_t h, uint64_t v) {
+  h ^= v + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+  return h * 0xBF58476D1CE4E5B9ull;
+}
+
+// Content fingerprint of n floats (see cached_model).
+uint64_t fingerprint(const float* p, size_t n, size_t row) {
+  if (!p) return 0;
+  const uint32_t* u = reinterpret_cast<const uint32_t*>(p);
+  uint64_t h = 0x1234567ull ^ n;
+  if (n <= (1u << 18)) {
+    for (size_t i = 0; i < n; ++i) h = mix64(h, u[i]);
+    return h;
+  }
+  const size_t samples = 1u << 16, stride = n / samples;
+  for (size_t i = 0; i < samples; ++i) h = mix64(h, u[i * stride]);
+  for (size_t i = 0; i < row && i < n; ++i) h = mix64(h, u[i]);
+  for (size_t i = n - std::min(row, n); i < n; ++i) h = mix64(h, u[i]);
+  return h;
+}
+
+struct ModelEntry {
+  const float* E;
+  uint32_t vocab;
+  int dim;
+  const float* bias;
+  uint64_t fp;
+  std::shared_ptr<lsb_model> m;
+};
+struct RecEntry {
+  const float* wh;
+  const float* we;
+  int dim;
+  uint64_t fp;
+  std::shared_ptr<lsb_recurrent> r;
+};
+constexpr size_t kCacheEntries = 4;
+
+}  // namespace
+
+std::shared_ptr<lsb_model> cached_model(const float* E, uint32_t vocab, int dim,
+                                        const float* bias) {
+  static std::vector<ModelEntry> cache;  // guarded by api_mutex (callers hold it)
+  const size_t n = static_cast<size_t>(vocab) * dim;
+  const uint64_t fp = mix64(fingerprint(E, n, dim), fingerprint(bias, vocab, 0));
+  for (size_t k = 0; k < cache.size(); ++k) {
+    ModelEntry& e = cache[k];
+    if (e.E == E && e.vocab == vocab && e.dim == dim && e.bias == bias && e.fp == fp) {
+      std::rotate(cache.begin(), cache.begin() + k, cache.begin() + k + 1);  // most recent first
+      return cache.front().m;
+    }
+  }
+  std::shared_ptr<lsb_model> m(upload_model(E, vocab, dim, bias).release(), ModelDeleter{});
+  cache.insert(cache.begin(), ModelEntry{E, vocab, dim, bias, fp, m});
+  if (cache.size() > kCacheEntries) cache.pop_back();
+  return m;
+}
+
+std::shared_ptr<lsb_recurrent> cached_recurrent(const float* wh, const float* we, int dim) {
+  static std::vector<RecEntry> cache;
+  const size_t n = static_cast<size_t>(dim) * dim;
+  const uint64_t fp = mix64(fingerprint(wh, n, dim), fingerprint(we, n, dim));
+  for (size_t k = 0; k < cache.size(); ++k) {
+    RecEntry& e = cache[k];
+    if (e.wh == wh && e.we == we && e.dim == dim && e.fp == fp) {
+      std::rotate(cache.begin(), cache.begin() + k, cache.begin() + k + 1);
+      return cache.front().r;
+    }
+  }
+  lsb_recurrent* r = nullptr;
+  check(lsb_recurrent_create(ctx(), wh, we, dim, &r), "recurrent upload");
+  std::shared_ptr<lsb_recurrent> sp(r, RecurrentDeleter{});
+  cache.insert(cache.begin(), RecEntry{wh, we, dim, fp, sp});
+  if (cache.size() > kCacheEntries) cache.pop_back();
+  return sp;
 }
 
 DevMem::DevMem(size_t bytes) { check(lsb_device_alloc(ctx(), bytes, &p), "device allocation"); }

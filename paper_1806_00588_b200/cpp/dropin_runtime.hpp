@@ -48,6 +48,16 @@ inline std::shared_ptr<lsb_index> share(lsb_index* i) {
 // Device copy of E (+ optional bias).
 ModelPtr upload_model(const float* E, uint32_t vocab, int dim, const float* bias);
 
+// Cached device copies for the per-call reference functions (gather_embeddings,
+// step_hidden, decode, build_lsh_index): the reference passes host matrices by
+// reference on every call, so the device copy is kept keyed by (host pointer,
+// shape) and a content fingerprint (every element up to 1 MB, else 64 Ki
+// evenly spaced samples plus the first and last rows), and re-uploaded when
+// either changes. A few entries, least recently used first out.
+std::shared_ptr<lsb_model> cached_model(const float* E, uint32_t vocab, int dim,
+                                        const float* bias);
+std::shared_ptr<lsb_recurrent> cached_recurrent(const float* wh, const float* we, int dim);
+
 // Device buffer owner.
 struct DevMem {
   void* p = nullptr;

@@ -533,7 +533,9 @@ static lsb_status launch_logits_survivors(lsb_ctx* ctx, LogitsArgs a, lsb_mode m
   // vocabulary): the one-lane-per-thread kernel of k_logits_ln.cu (same bits;
   // B200 cfg-2 shapes, S = 16 / 64 / 128: 588 / 2265 / 4606 us vs 633 / 2696 /
   // 5328 us here). With per-sentence survivors it measured slower (108-125 vs
-  // 100 us at cfg 2), so the LSH step keeps the tiles below.
+  // 100 us at cfg 2), and so did the cfg-2 shared block alone on it beside
+  // the survivor tiles on a second stream (119 vs 102 us: 512 CTAs, under one
+  // wave, no steady state), so the LSH step keeps the tiles below.
   static const int ln_mode = getenv("LSB_K4_LN") ? atoi(getenv("LSB_K4_LN")) : 1;
   if (!fast && ln_mode && logits_ln_applies(a) &&
       (ln_mode == 2 || (!a.ids && a.R_total > 12 && a.n_shared >= 4096)))
