@@ -488,11 +488,35 @@ def run_extras(ctx, model, idx, Hd, sc, fin, nh, choices, nchoice, hout, args, l
         return timer(lambda k: b.step(base + (k % c["inputs"]) * step_bytes, sc, fin, nh,
                                       choices, nchoice, hout), steps)
 
+    tf32_peak = measured_tf32_peak()
     for nm, mode in [("full_vocab_parity", PARITY), ("full_vocab_fast", FAST)]:
         b = Batch(ctx, model, None, S=S, B=B, specials=[V - 1], mode=mode, full_vocab=True)
         ms = time_batch(b, 5)
+        b.profile(True, every=1)
+        for k in range(5):
+            b.step(base + k * step_bytes, sc, fin, nh, choices, nchoice, hout)
+        st, nrec = b.stage_totals()
+        b.profile(False)
+        stg = {k: round(float(v) / max(nrec, 1), 4) for k, v in
+               zip(["probe_count", "compact", "logits", "softmax_topb", "expand"], st)}
         out[nm] = {"ms_per_step": round(ms, 4), "value": round(S / (ms / 1e3), 1),
-                   "lsh_speedup": round(lsh_value / (S / (ms / 1e3)), 2)}
+                   "lsh_speedup": round(lsh_value / (S / (ms / 1e3)), 2), "stage_ms": stg}
+        macs = float(S * B) * V * d
+        if mode == PARITY:
+            peak = ctx.fp32x2_peak()
+            ach = 2.0 * macs / (stg["logits"] / 1e3)
+            out[nm]["roofline"] = {"kernel": "k_logits_ln", "bound": "fp32",
+                                   "achieved": round(ach / 1e12, 3), "peak": round(peak / 1e12, 3),
+                                   "unit": "T FP32 lane-ops/s", "frac": round(ach / peak, 4)}
+        else:
+            # 3xTF32: three tensor-core products per MAC (hi*hi + hi*lo + lo*hi)
+            ach = 3.0 * 2.0 * macs / (stg["logits"] / 1e3)
+            out[nm]["roofline"] = {"kernel": "k_tc_logits", "bound": "tensor",
+                                   "achieved": round(ach / 1e12, 1),
+                                   "peak": round(tf32_peak / 1e12, 1), "unit": "TFLOP/s (tf32)",
+                                   "frac": round(ach / tf32_peak, 4),
+                                   "peak_kind": "measured in this run: torch.matmul TF32 "
+                                                "(cuBLAS) 8192^3, best of 5"}
         b.close()
     other = FAST if args.mode == "parity" else PARITY
     bo = Batch(ctx, model, idx, S=S, B=B, T=c["T"], t=c["t"], specials=[V - 1], mode=other)
@@ -534,6 +558,32 @@ def run_extras(ctx, model, idx, Hd, sc, fin, nh, choices, nchoice, hout, args, l
     out["cfg1"] = run_cfg1(ctx, model, idx, c)
     out["operating_point"] = run_operating_point(ctx)
     return out
+
+
+def measured_tf32_peak():
+    """Dense TF32 tensor-core throughput of this GPU (cuBLAS via torch.matmul
+    with TF32 allowed, 8192^3, best of 5): the denominator of the FAST
+    full-vocabulary GEMM's roofline."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        n = 8192
+        a = torch.randn(n, n, device="cuda")
+        b = torch.randn(n, n, device="cuda")
+        torch.matmul(a, b)
+        best = 1e30
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b
+        return 2.0 * n ** 3 / (best / 1e3)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
 
 
 def run_cfg1(ctx, model, idx, c):

@@ -535,7 +535,10 @@ static lsb_status launch_logits_survivors(lsb_ctx* ctx, LogitsArgs a, lsb_mode m
   // 5328 us here). With per-sentence survivors it measured slower (108-125 vs
   // 100 us at cfg 2), and so did the cfg-2 shared block alone on it beside
   // the survivor tiles on a second stream (119 vs 102 us: 512 CTAs, under one
-  // wave, no steady state), so the LSH step keeps the tiles below.
+  // wave, no steady state), so the LSH step keeps the tiles below. (Also
+  // measured: the top-T block started on a side stream at the step's start,
+  // overlapping K1-K3: 500 k vs 508 k sentence-steps/s -- the FP-bound block
+  // takes the SM slots the latency-bound probe needs.)
   static const int ln_mode = getenv("LSB_K4_LN") ? atoi(getenv("LSB_K4_LN")) : 1;
   if (!fast && ln_mode && logits_ln_applies(a) &&
       (ln_mode == 2 || (!a.ids && a.R_total > 12 && a.n_shared >= 4096)))
