@@ -104,6 +104,9 @@ constexpr size_t kCacheEntries = 4;
 
 std::shared_ptr<lsb_model> cached_model(const float* E, uint32_t vocab, int dim,
                                         const float* bias) {
+  // the context first: function-local statics are destroyed in reverse order
+  // of construction, so the cached device copies are freed before it
+  ctx();
   static std::vector<ModelEntry> cache;  // guarded by api_mutex (callers hold it)
   const size_t n = static_cast<size_t>(vocab) * dim;
   const uint64_t fp = mix64(fingerprint(E, n, dim), fingerprint(bias, vocab, 0));
@@ -121,6 +124,7 @@ std::shared_ptr<lsb_model> cached_model(const float* E, uint32_t vocab, int dim,
 }
 
 std::shared_ptr<lsb_recurrent> cached_recurrent(const float* wh, const float* we, int dim) {
+  ctx();  // constructed before the cache (see cached_model)
   static std::vector<RecEntry> cache;
   const size_t n = static_cast<size_t>(dim) * dim;
   const uint64_t fp = mix64(fingerprint(wh, n, dim), fingerprint(we, n, dim));

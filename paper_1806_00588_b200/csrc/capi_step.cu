@@ -143,6 +143,10 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
   if (cfg->B < 1) return set_error("config: beam must be >= 1"), LSB_EINVAL;
   if (cfg->B > 64) return set_error("config: beam above 64 is not supported by the fused step"), LSB_EINVAL;
   if (cfg->S < 1) return set_error("config: at least one sentence"), LSB_EINVAL;
+  // the gather kernels address E rows by 32-bit element offsets (bit 31 marks
+  // a padding column)
+  if (static_cast<uint64_t>(V) * model->d >= (1ull << 31))
+    return set_error("lsb_batch_create: |V| x d must stay below 2^31 elements"), LSB_EINVAL;
   if (cfg->top_merge > V) return set_error("config: T exceeds vocabulary size"), LSB_EINVAL;
   if (!cfg->full_vocab && !cfg->top_only) {
     if (!idx || !idx->has_perms)
@@ -221,7 +225,8 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
     const int R = static_cast<int>(SB);
     int G = 0;
     if (split_env > 0) G = split_env;
-    else if (split_env < 0 && b->idx->W > 64 && static_cast<long>(R) * nslices < ctx->sm_count)
+    else if (split_env < 0 && b->idx->W > 64 && b->idx->W <= 65535 &&  // 16-bit counts <= W
+             static_cast<long>(R) * nslices < ctx->sm_count)
       G = (2 * ctx->sm_count + R - 1) / R;
     G = std::min(G, b->idx->W);
     const uint32_t words = ((V + 1) / 2 + 3) & ~3u;
