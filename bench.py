@@ -64,6 +64,9 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     p.add_argument("--mode", default="parity", choices=["parity", "fast"])
+    p.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                   help="cfg4 at N > 1: device pushes into peer memory (CUDA IPC) or NCCL "
+                        "all-gathers")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-extras", action="store_true", help="skip the same-GPU comparison legs")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -232,6 +235,12 @@ def run_ours(args, rank, world, local):
         shard = VocabShard(ctx, Es, bs, v0, V, c["K"], c["u"], c["W"], ps, isd, S, B, c["T"],
                            c["t"], specials=[V - 1], mode=mode)
         model, idx, batch = shard.model, shard.index, shard.batch
+        xchg = None
+        if args.exchange == "peer":
+            from paper_1806_00588_b200.vocab_shard import PeerExchange
+            xchg = PeerExchange(shard, world, rank)
+            xchg.connect()
+            torch.distributed.barrier()
     else:
         Ed, bd = E.cuda(), bias.cuda()
         torch.cuda.synchronize()
@@ -251,7 +260,10 @@ def run_ours(args, rank, world, local):
     base = Hd.data_ptr()
     torch.cuda.synchronize()
 
-    if vsh:
+    if vsh and xchg is not None:
+        def step(k):
+            xchg.step(Hd[k % c["inputs"]], sc, fin, nh, choices, nchoice, hout)
+    elif vsh:
         def step(k):
             with torch.cuda.stream(stream):
                 sharded_step(shard, Hd[k % c["inputs"]], sc, fin, nh, choices, nchoice, hout)
@@ -346,7 +358,7 @@ def run_ours(args, rank, world, local):
         e2e = time_e2e_leg(args, batch, H, scores, S, B, d, world, coll_dev, S_job)
     else:
         e2e = time_e2e_sharded(args, shard, sharded_step, H, scores, S, B, d, world, coll_dev,
-                               S_job, stream)
+                               S_job, stream, xchg)
 
     extras = {}
     if not args.no_extras and rank == 0 and world == 1 and name == "cfg2":
@@ -367,7 +379,9 @@ def run_ours(args, rank, world, local):
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(name, E, bias, H, scores, args.cpu_seconds)
     if world > 1:
-        torch.distributed.barrier()
+        torch.distributed.barrier()  # no rank still pushes into a peer's area
+        if vsh and xchg is not None:
+            xchg.close()
         torch.distributed.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -431,7 +445,7 @@ def time_e2e_leg(args, batch, H, scores, S, B, d, world, coll_dev, S_job):
 
 
 def time_e2e_sharded(args, shard, sharded_step, H, scores, S, B, d, world, coll_dev, S_job,
-                     stream):
+                     stream, xchg=None):
     """Vocabulary-sharded e2e: per step the host inputs are uploaded from pinned
     memory, the sharded step runs (NCCL exchanges included) and rank 0 reads
     the choices back."""
@@ -450,7 +464,10 @@ def time_e2e_sharded(args, shard, sharded_step, H, scores, S, B, d, world, coll_
         with torch.cuda.stream(stream):
             Hd.copy_(Hh[k % n_in], non_blocking=True)
             sc.copy_(sch, non_blocking=True)
-            sharded_step(shard, Hd, sc, fin, nh, ch, nc, None)
+            if xchg is not None:
+                xchg.step(Hd, sc, fin, nh, ch, nc, None)
+            else:
+                sharded_step(shard, Hd, sc, fin, nh, ch, nc, None)
             ch_h.copy_(ch, non_blocking=True)
         stream.synchronize()
 
@@ -467,8 +484,10 @@ def time_e2e_sharded(args, shard, sharded_step, H, scores, S, B, d, world, coll_
     el = float(t.item())
     return {"value": round(S_job * n_e2e / el, 1), "unit": UNIT, "steps": n_e2e,
             "h2d_bytes_per_step": S * B * d * 4 + S * B * 8, "d2h_bytes_per_step": S * B * 24,
-            "api": "vocab_shard.sharded_step (C ABI phases + NCCL all-gathers), one host sync "
-                   "per step"}
+            "api": ("lsb_shard_step_peer (C ABI: phases + pushes into peer memory + device flag "
+                    "waits)" if xchg is not None else
+                    "vocab_shard.sharded_step (C ABI phases + NCCL all-gathers)")
+                   + ", one host sync per step"}
 
 
 def run_extras(ctx, model, idx, Hd, sc, fin, nh, choices, nchoice, hout, args, lsh_value, c):

@@ -379,6 +379,28 @@ lsb_status lsb_shard_phase3(lsb_batch* b, const lsb_state_dev* in, const double*
 lsb_status lsb_shard_phase3_packed(lsb_batch* b, const lsb_state_dev* in, const void* packed_dev,
                                    int G, const lsb_out_dev* out);
 
+/* The same step with the exchange over PEER MEMORY instead of collectives
+ * (NVLink / NVSwitch between the GPUs of a node, CUDA IPC between processes):
+ * each rank creates an exchange area, publishes its 64-byte IPC handle, opens
+ * every peer's (or, for ranks in one process, attaches their areas with
+ * lsb_shard_xchg_set_peer), then lsb_shard_step_peer runs phase 1, pushes its
+ * row maxima into every peer's area and waits on per-rank sequence flags on
+ * the device, runs phase 2, pushes the packed sums + lists, waits, and runs
+ * phase 3 -- no host synchronisation and no collective call per step. The
+ * ranks' streams must be able to run concurrently (one process per GPU, or
+ * separate streams of one GPU); ranks that share ONE process must use eager
+ * CUDA module loading (CUDA_MODULE_LOADING=EAGER), since a lazy kernel load
+ * on the host thread would wait for that process's spinning flag wait. */
+typedef struct lsb_shard_xchg lsb_shard_xchg;
+lsb_status lsb_shard_xchg_create(lsb_batch* b, int G, int rank, lsb_shard_xchg** out);
+lsb_status lsb_shard_xchg_destroy(lsb_shard_xchg* x);
+void* lsb_shard_xchg_area(lsb_shard_xchg* x);
+lsb_status lsb_shard_xchg_ipc_handle(lsb_shard_xchg* x, void* handle64);
+lsb_status lsb_shard_xchg_open_ipc(lsb_shard_xchg* x, int peer, const void* handle64);
+lsb_status lsb_shard_xchg_set_peer(lsb_shard_xchg* x, int peer, void* area_dev);
+lsb_status lsb_shard_step_peer(lsb_batch* b, lsb_shard_xchg* x, const lsb_state_dev* in,
+                               uint32_t word_base, const lsb_out_dev* out);
+
 #ifdef __cplusplus
 }
 #endif

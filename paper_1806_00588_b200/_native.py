@@ -136,6 +136,14 @@ _SIGS = [
                                    C.POINTER(lsb_out_dev)]),
     ("lsb_shard_phase3_packed", C.c_int, [VP, C.POINTER(lsb_state_dev), VP, C.c_int,
                                           C.POINTER(lsb_out_dev)]),
+    ("lsb_shard_xchg_create", C.c_int, [VP, C.c_int, C.c_int, C.POINTER(VP)]),
+    ("lsb_shard_xchg_destroy", C.c_int, [VP]),
+    ("lsb_shard_xchg_area", VP, [VP]),
+    ("lsb_shard_xchg_ipc_handle", C.c_int, [VP, VP]),
+    ("lsb_shard_xchg_open_ipc", C.c_int, [VP, C.c_int, VP]),
+    ("lsb_shard_xchg_set_peer", C.c_int, [VP, C.c_int, VP]),
+    ("lsb_shard_step_peer", C.c_int, [VP, VP, C.POINTER(lsb_state_dev), U32,
+                                      C.POINTER(lsb_out_dev)]),
 ]
 
 EXPORTED = [s[0] for s in _SIGS]

@@ -95,4 +95,6 @@ namespace lsb {
 // K1+K2 -> K3 -> K4 of one step (profiling events 0..3): candidate sets in
 // b->ids / b->n_cand, logits in b->logits.
 lsb_status step_front(lsb_batch* b, const lsb_state_dev* in, int empty_is_error);
+// Vocabulary-sharded step: phase-2 scratch (capi_shard.cu).
+lsb_status ensure_shard_scratch(lsb_batch* b, int G);
 }  // namespace lsb

@@ -172,9 +172,10 @@ __global__ void __launch_bounds__(kShT) k_shard_combine(const double* __restrict
 
 using namespace lsb;
 
-namespace {
-
-lsb_status ensure_shard_scratch(lsb_batch* b, int G) {
+// Allocates the phase-2 scratch of a shard batch (first phase-2 call, or
+// up front: the peer exchange must not allocate -- cudaMalloc synchronises the
+// device while a flag-wait kernel may be spinning on another rank's push).
+lsb_status lsb::ensure_shard_scratch(lsb_batch* b, int G) {
   const size_t R = static_cast<size_t>(b->S) * b->B;
   const int Bp = b->B + kShardSlack;
   if (!b->sh_top) {
@@ -184,6 +185,8 @@ lsb_status ensure_shard_scratch(lsb_batch* b, int G) {
   (void)G;
   return LSB_OK;
 }
+
+namespace {
 
 bool live_args(const lsb_batch* b, const lsb_state_dev* in) {
   return b && in && in->hidden && in->scores;

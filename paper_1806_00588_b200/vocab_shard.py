@@ -107,6 +107,66 @@ class VocabShard:
             x.close()
 
 
+class PeerExchange:
+    """The step's exchange over peer memory (lsb_shard_xchg, capi_xchg.cu): an
+    exchange area per rank, attached to every other rank's -- through CUDA IPC
+    handles across processes (NVLink / NVSwitch between GPUs), or directly for
+    shards held by one process -- then ``step`` runs the three phases with
+    device-side pushes and sequence-flag waits, no collective per step."""
+
+    def __init__(self, shard: "VocabShard", G: int, rank: int):
+        self.shard, self.lib, self.G, self.rank = shard, shard.lib, G, rank
+        h = C.c_void_p()
+        N.check(self.lib.lsb_shard_xchg_create(shard.batch.h, G, rank, C.byref(h)),
+                "lsb_shard_xchg_create")
+        self.h = h
+
+    @property
+    def area(self) -> int:
+        return int(self.lib.lsb_shard_xchg_area(self.h))
+
+    def ipc_handle(self) -> bytes:
+        buf = (C.c_uint8 * 64)()
+        N.check(self.lib.lsb_shard_xchg_ipc_handle(self.h, buf), "lsb_shard_xchg_ipc_handle")
+        return bytes(buf)
+
+    def open_ipc(self, peer: int, handle: bytes):
+        buf = (C.c_uint8 * 64).from_buffer_copy(handle)
+        N.check(self.lib.lsb_shard_xchg_open_ipc(self.h, peer, buf), "lsb_shard_xchg_open_ipc")
+
+    def set_peer(self, peer: int, area: int):
+        N.check(self.lib.lsb_shard_xchg_set_peer(self.h, peer, C.c_void_p(area)),
+                "lsb_shard_xchg_set_peer")
+
+    def connect(self, group=None):
+        """Across processes: all-gather the IPC handles once (any backend) and
+        open every peer's area."""
+        import torch
+        import torch.distributed as dist
+        mine = torch.frombuffer(bytearray(self.ipc_handle()), dtype=torch.uint8)
+        if dist.get_backend(group) == "nccl":
+            mine = mine.cuda()
+        allh = torch.empty(self.G * 64, dtype=torch.uint8, device=mine.device)
+        dist.all_gather_into_tensor(allh, mine, group=group)
+        allh = allh.cpu().numpy().tobytes()
+        for g in range(self.G):
+            if g != self.rank:
+                self.open_ipc(g, allh[64 * g:64 * (g + 1)])
+
+    def step(self, hidden, scores, finished, n_hyp, choices, n_choices, hidden_out=None):
+        st = self.shard._state(hidden, scores, finished, n_hyp)
+        out = N.lsb_out_dev(choices.data_ptr(), n_choices.data_ptr(),
+                            hidden_out.data_ptr() if hidden_out is not None else None)
+        N.check(self.lib.lsb_shard_step_peer(self.shard.batch.h, self.h, C.byref(st),
+                                             self.shard.v0, C.byref(out)),
+                "lsb_shard_step_peer")
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.lsb_shard_xchg_destroy(self.h)
+            self.h = None
+
+
 def _gather(x, G: int, group):
     """all_gather in rank order into a flat buffer (the layout gloo and NCCL
     both accept), viewed as [G, *x.shape]. Under gloo (the CPU tests, or

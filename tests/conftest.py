@@ -11,6 +11,11 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+def pytest_addoption(parser):
+    parser.addoption("--run-peer-inprocess", action="store_true", default=False,
+                     help="run the in-process peer-exchange cases (needs CUDA_MODULE_LOADING=EAGER)")
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and liblshbeam_b200.so")
 

@@ -27,7 +27,7 @@ def _inputs():
     return E, bias, H, scores, finished, n_hyp
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, peer=False):
     import torch
     import torch.distributed as dist
 
@@ -49,7 +49,20 @@ def _worker(rank, world, port, q):
         ch = torch.zeros(S * B * 24, dtype=torch.uint8, device=dev)
         nc = torch.zeros(S, dtype=torch.int32, device=dev)
         ho = torch.zeros(S, B, D, device=dev)
-        sharded_step(shard, H.cuda(), scores.cuda(), finished.cuda(), n_hyp.cuda(), ch, nc, ho)
+        if peer:
+            # peer-memory exchange: CUDA IPC areas, handles all-gathered once
+            from paper_1806_00588_b200.vocab_shard import PeerExchange
+            x = PeerExchange(shard, world, rank)
+            x.connect()
+            dist.barrier()
+            for _ in range(2):  # two steps: the sequence flags advance
+                x.step(H.cuda(), scores.cuda(), finished.cuda(), n_hyp.cuda(), ch, nc, ho)
+                ctx.sync()
+            dist.barrier()  # no peer may still push into our area
+            x.close()
+        else:
+            sharded_step(shard, H.cuda(), scores.cuda(), finished.cuda(), n_hyp.cuda(), ch, nc,
+                         ho)
         ctx.sync()
         q.put((rank, ch.cpu().numpy().tobytes(), nc.cpu().numpy().tolist(),
                ho.cpu().numpy().tobytes()))
@@ -58,7 +71,8 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_process_vocab_sharded_cuda_step(ctx):
+@pytest.mark.parametrize("peer", [False, True])
+def test_two_process_vocab_sharded_cuda_step(ctx, peer):
     import torch
     import torch.multiprocessing as mp
 
@@ -69,7 +83,7 @@ def test_two_process_vocab_sharded_cuda_step(ctx):
         port = s.getsockname()[1]
     mctx = mp.get_context("spawn")
     q = mctx.Queue()
-    procs = [mctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [mctx.Process(target=_worker, args=(r, 2, port, q, peer)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted(q.get(timeout=300) for _ in procs)
