@@ -49,7 +49,7 @@ WORKLOADS = {
                  desc="cfg3: large beam B=50, 256 sentences split over the GPUs, |V|=40000, "
                       "d=1000, K=8 u=3 W=16, T=1000, t=2"),
     "cfg4": dict(V=200000, d=1024, B=12, S=64, K=8, u=3, W=16, T=1000, t=2, seed=7, inputs=8,
-                 scaling="strong",
+                 scaling="strong", vocab_sharded=True,
                  desc="cfg4: large vocabulary |V|=200000, d=1024, B=12, 64 sentences, "
                       "vocabulary-sharded over the GPUs (NCCL top-B merge), K=8 u=3 W=16, "
                       "T=1000, t=2"),
@@ -64,9 +64,10 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     p.add_argument("--mode", default="parity", choices=["parity", "fast"])
-    p.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
-                   help="cfg4 at N > 1: device pushes into peer memory (CUDA IPC) or NCCL "
-                        "all-gathers")
+    p.add_argument("--exchange", default="auto", choices=["auto", "peer", "nccl"],
+                   help="cfg4 at N > 1: device pushes into peer memory (CUDA IPC / NVLink) or "
+                        "collective all-gathers; auto = peer with one GPU per rank, collectives "
+                        "when ranks share GPUs (time-sliced processes make spin waits slow)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-extras", action="store_true", help="skip the same-GPU comparison legs")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -236,7 +237,7 @@ def run_ours(args, rank, world, local):
                            c["t"], specials=[V - 1], mode=mode)
         model, idx, batch = shard.model, shard.index, shard.batch
         xchg = None
-        if args.exchange == "peer":
+        if args.exchange == "peer" or (args.exchange == "auto" and world <= ngpu):
             from paper_1806_00588_b200.vocab_shard import PeerExchange
             xchg = PeerExchange(shard, world, rank)
             xchg.connect()
