@@ -68,9 +68,11 @@ struct lsb_batch {
     lsb_choice* choices = nullptr;
     int32_t* n_choices = nullptr;
     cudaEvent_t uploaded = nullptr, computed = nullptr, consumed = nullptr;
+    cudaEvent_t uploaded2 = nullptr;  // second half of the hidden states
     bool used = false;
   } slot[2];
   cudaStream_t copy_stream = nullptr;   // uploads
+  cudaStream_t copy_stream2 = nullptr;  // second copy engine: half of each hidden upload
   cudaStream_t down_stream = nullptr;   // read-backs
   int next_slot = 0;
   // CUDA graph of one lsb_step on fixed device buffers (lsb_batch_graph_*)
