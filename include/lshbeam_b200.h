@@ -237,7 +237,7 @@ lsb_status lsb_step_host(lsb_batch* b, const lsb_state_host* in, lsb_choice* cho
                          int32_t* n_choices_host, float* hidden_out_host);
 
 /* Pipelined form of lsb_step_host for a stream of steps: enqueues the
- * uploads on an internal copy stream (two staging slots, so step k+1's
+ * uploads on internal copy streams (three staging slots, so step k+1's
  * upload overlaps step k's kernels), the step, and the read-back of the
  * choices into the caller's (pinned) buffers; does not synchronise. The
  * host buffers must stay valid until lsb_batch_wait returns. */

@@ -58,7 +58,7 @@ struct lsb_batch {
   lsb_choice* h_choices = nullptr;
   int32_t* h_nchoices = nullptr;
   float* h_hidden_out = nullptr;
-  // pipelined host-buffer steps (lsb_step_host_async): two staging slots, a
+  // pipelined host-buffer steps (lsb_step_host_async): three staging slots, a
   // copy stream for the uploads, events ordering uploads and kernels
   struct AsyncSlot {
     float* hidden = nullptr;
@@ -70,7 +70,8 @@ struct lsb_batch {
     cudaEvent_t uploaded = nullptr, computed = nullptr, consumed = nullptr;
     cudaEvent_t uploaded2 = nullptr;  // second half of the hidden states
     bool used = false;
-  } slot[2];
+  } slot[3];
+  static constexpr int kSlots = 3;  // an upload waits on the step three calls back
   cudaStream_t copy_stream = nullptr;   // uploads
   cudaStream_t copy_stream2 = nullptr;  // second copy engine: half of each hidden upload
   cudaStream_t down_stream = nullptr;   // read-backs

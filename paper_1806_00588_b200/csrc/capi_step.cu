@@ -462,7 +462,7 @@ lsb_status lsb_step_host(lsb_batch* b, const lsb_state_host* in, lsb_choice* cho
 }
 
 // Pipelined variant of lsb_step_host: uploads go to an upload stream into
-// one of two staging slots while the previous step's kernels run; the step
+// one of three staging slots while the previous step's kernels run; the step
 // waits for its upload; its choices are read back on a third stream, so the
 // step stream runs kernels only.
 // Nothing synchronises the host; lsb_batch_wait drains the pipeline.
@@ -492,9 +492,9 @@ lsb_status lsb_step_host_async(lsb_batch* b, const lsb_state_host* in, lsb_choic
     }
   }
   auto& sl = b->slot[b->next_slot];
-  b->next_slot ^= 1;
+  b->next_slot = (b->next_slot + 1) % lsb_batch::kSlots;
   cudaStream_t cs = b->copy_stream;
-  // the step that used this slot two calls ago must be done reading it
+  // the step that used this slot three calls ago must be done reading it
   cudaStream_t cs2 = b->copy_stream2;
   if (sl.used) {
     LSB_CUDA(cudaStreamWaitEvent(cs, sl.consumed, 0));
