@@ -438,6 +438,7 @@ lsb_status lsb_index_import(lsb_ctx* ctx, uint32_t vocab, int W, const uint32_t*
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(idx->perms, idx->perms_host.data(), idx->perms_host.size() * 4,
                           cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = upload_perms16(idx, st);
     if (e != cudaSuccess) return fail(e, "lsb_index_import perms");
     idx->has_perms = true;
   }

@@ -349,6 +349,23 @@ __global__ void k_find_batch(IndexView ix, const int32_t* __restrict__ bands,
 
 // ------------------------------------------------------------ host side
 // PermutationSet::generate, src/wta_hash.cpp:31-55 (host, bit-exact).
+cudaError_t upload_perms16(lsb_index* idx, cudaStream_t st) {
+  if (idx->dim > 65535 || idx->K < 1 || idx->perms_host.empty()) return cudaSuccess;
+  const int K16 = (idx->K + 7) & ~7;
+  std::vector<uint16_t> h(static_cast<size_t>(idx->P) * K16, 0);
+  for (int p = 0; p < idx->P; ++p)
+    for (int k = 0; k < idx->K; ++k)
+      h[static_cast<size_t>(p) * K16 + k] =
+          static_cast<uint16_t>(idx->perms_host[static_cast<size_t>(p) * idx->K + k]);
+  cudaError_t e = cudaMalloc(&idx->perms16, h.size() * sizeof(uint16_t));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(idx->perms16, h.data(), h.size() * sizeof(uint16_t),
+                        cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // h is a stack temporary
+  if (e == cudaSuccess) idx->K16 = K16;
+  return e;
+}
+
 static void generate_perms_host(int d, int P, int K, uint64_t seed, std::vector<uint32_t>& out) {
   out.assign(static_cast<size_t>(P) * K, 0);
   std::vector<uint32_t> scratch(d);
@@ -541,6 +558,7 @@ extern "C" {
 lsb_status lsb_index_destroy(lsb_index* idx) {
   if (!idx) return LSB_OK;
   if (idx->perms) cudaFree(idx->perms);
+  if (idx->perms16) cudaFree(idx->perms16);
   if (idx->word_ids) cudaFree(idx->word_ids);
   if (idx->slots) cudaFree(idx->slots);
   if (idx->bands) cudaFree(idx->bands);
@@ -581,6 +599,8 @@ lsb_status lsb_index_build(lsb_ctx* ctx, const lsb_model* model, int K, int u, i
   e = cudaMemcpyAsync(idx->perms, idx->perms_host.data(), idx->perms_host.size() * 4,
                       cudaMemcpyHostToDevice, ctx->stream);
   if (e != cudaSuccess) return fail(cuda_status(e, "upload perms"));
+  e = upload_perms16(idx, ctx->stream);
+  if (e != cudaSuccess) return fail(cuda_status(e, "upload perms16"));
   DevBuf<uint32_t> codes;
   e = codes.alloc(static_cast<size_t>(model->V) * W, ctx->stream);
   if (e != cudaSuccess) return fail(cuda_status(e, "cudaMalloc codes"));

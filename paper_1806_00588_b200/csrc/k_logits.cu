@@ -539,6 +539,10 @@ static lsb_status launch_logits_survivors(lsb_ctx* ctx, LogitsArgs a, lsb_mode m
   // measured: the top-T block started on a side stream at the step's start,
   // overlapping K1-K3: 500 k vs 508 k sentence-steps/s -- the FP-bound block
   // takes the SM slots the latency-bound probe needs.)
+  // (On the LSH step it wins only with many survivors per sentence: d = 256
+  // and ~2470 survivors, S = 64: 75.8 vs 100.4 us; with the operating point's
+  // ~400 candidates it lost, 0.146 vs 0.132 ms per step: survivor counts are
+  // only known on the device, so the LSH step keeps the tiles below.)
   static const int ln_mode = getenv("LSB_K4_LN") ? atoi(getenv("LSB_K4_LN")) : 1;
   if (!fast && ln_mode && logits_ln_applies(a) &&
       (ln_mode == 2 || (!a.ids && a.R_total > 12 && a.n_shared >= 4096)))

@@ -105,10 +105,24 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(
     // more permutations than threads (large W): each thread's permutation
     // rows are fetched whole (K loads in flight), not one load per step
     for (int p = threadIdx.x; p < ix.P; p += blockDim.x) {
-      const uint32_t* pr = ix.perms + static_cast<size_t>(p) * ix.K;
       uint32_t q[kMaxKReg];
+      if (ix.perms16) {  // 8 uint16 indices per 16-byte load (2 loads at K = 16, not 16)
+        const uint4* pr = reinterpret_cast<const uint4*>(ix.perms16 + static_cast<size_t>(p) * ix.K16);
 #pragma unroll
-      for (int k = 0; k < kMaxKReg; ++k) q[k] = k < ix.K ? __ldg(pr + k) : 0u;
+        for (int c = 0; c < kMaxKReg / 8; ++c) {
+          const uint4 v = c * 8 < ix.K ? __ldg(pr + c) : make_uint4(0, 0, 0, 0);
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int h2 = 0; h2 < 4; ++h2) {
+            q[c * 8 + 2 * h2] = w[h2] & 0xFFFFu;
+            q[c * 8 + 2 * h2 + 1] = w[h2] >> 16;
+          }
+        }
+      } else {
+        const uint32_t* pr = ix.perms + static_cast<size_t>(p) * ix.K;
+#pragma unroll
+        for (int k = 0; k < kMaxKReg; ++k) q[k] = k < ix.K ? __ldg(pr + k) : 0u;
+      }
       uint32_t best = 0;
       float bv = h[q[0]];
 #pragma unroll

@@ -44,10 +44,15 @@ struct IndexView {
   const BandMeta* bands;     // W
   uint32_t V;
   int W, K, u, bits, P, d;
+  const uint16_t* perms16;   // P x K16 (K padded to a multiple of 8), or null
+  int K16;
 };
 
 // ----------------------------------------------------------- host state
 void set_error(const std::string& msg);
+// Uploads idx->perms_host as the uint16 copy the probe kernels read with
+// 16-byte loads (perms16, row stride K16 = K rounded up to 8); no-op for d > 65535.
+cudaError_t upload_perms16(lsb_index* idx, cudaStream_t st);
 lsb_status cuda_status(cudaError_t e, const char* what);
 // Raises `func`'s dynamic shared-memory limit to at least `bytes` on the
 // context's device. cudaFuncSetAttribute is per device, so the configured size
@@ -92,6 +97,8 @@ struct lsb_index {
   bool has_perms = false;
   uint64_t perm_seed = 0, index_seed = 0;
   uint32_t* perms = nullptr;     // P x K (device)
+  uint16_t* perms16 = nullptr;   // P x K16 (device, d <= 65535): 16-byte loads of 8 indices
+  int K16 = 0;
   uint32_t* word_ids = nullptr;  // W x V (device)
   uint4* slots = nullptr;        // total_slots (device)
   lsb::BandMeta* bands = nullptr;  // W (device)
@@ -102,7 +109,7 @@ struct lsb_index {
   uint32_t attempts = 0;
 
   lsb::IndexView view() const {
-    return lsb::IndexView{perms, word_ids, slots, bands, V, W, K, u, bits, P, dim};
+    return lsb::IndexView{perms, word_ids, slots, bands, V, W, K, u, bits, P, dim, perms16, K16};
   }
 };
 
