@@ -217,10 +217,10 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
   // Few rows with many bands (a one-sentence decode at W > 64): k_probe_count
   // would run S*B CTAs on a 148-SM GPU, each walking every band's span; split
   // each row's bands over G CTAs (k_probe_split) so the grid covers ~2 CTAs
-  // per SM. Measured at S=1, V=50k, W=500: K=8 (98-word spans) 100 -> 29 us,
-  // K=16 (12-word spans) 35 -> 33 us; at W=16 (cfg 1) it was slower (16.7 vs
-  // 10.8 us: global-counter atomics vs shared-memory ones), so W <= 64 keeps
-  // k_probe_count. LSB_PROBE_SPLIT=0 turns it off, =G forces G.
+  // per SM. Measured at S=1, V=50k, W=500: K=8 (98-word spans) 100 -> 29 us;
+  // with short spans (K=16: 12 words) and at W=16 (cfg 1: 16.7 vs 10.8 us,
+  // global-counter atomics vs shared-memory ones) k_probe_count stays faster.
+  // LSB_PROBE_SPLIT=0 turns it off, =G forces G.
   if (e == cudaSuccess && b->idx && b->t > 0) {
     static const int split_env = getenv("LSB_PROBE_SPLIT") ? atoi(getenv("LSB_PROBE_SPLIT")) : -1;
     const uint32_t nslices = b->slice_len ? (V + b->slice_len - 1) / b->slice_len : 1;
@@ -228,7 +228,11 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
     int G = 0;
     if (split_env > 0) G = split_env;
     else if (split_env < 0 && b->idx->W > 64 && b->idx->W <= 65535 &&  // 16-bit counts <= W
-             static_cast<long>(R) * nslices < ctx->sm_count)
+             static_cast<long>(R) * nslices < ctx->sm_count &&
+             // long spans only: with ~12-word spans (K=16, u=3: 12-bit codes)
+             // k_probe_count is faster (26 vs 33 us at S=1, V=50k, W=500)
+             (b->idx->u * b->idx->bits >= 32 ||
+              (static_cast<uint64_t>(V) >> (b->idx->u * b->idx->bits)) >= 32))
       G = (2 * ctx->sm_count + R - 1) / R;
     G = std::min(G, b->idx->W);
     const uint32_t words = ((V + 1) / 2 + 3) & ~3u;
