@@ -61,6 +61,10 @@ CASES = [
     (4000, 64, 4, 2, 8, 2, 24, 100, 1),
     # rows longer than the register path (n > 3072): global threshold path
     (8000, 64, 8, 3, 16, 2, 12, 4000, 2),
+    # few rows x many bands with long spans (4-bit codes over 20k words):
+    # the band-split probe (k_probe_split, 16-bit counters in L2)
+    (20000, 32, 4, 2, 100, 2, 12, 100, 3),
+    (12000, 48, 4, 2, 80, 1, 7, 40, 5),
     # t = 0 over V >= 8192: every row is the whole vocabulary -> segmented K5a
     (9000, 32, 8, 3, 16, 2, 6, 0, 0),
     (12000, 16, 4, 2, 8, 1, 40, 0, 0),
