@@ -22,6 +22,10 @@ namespace lsb {
 
 // =================================================================== K1+K2
 constexpr int kWarpBands = 64;  // up to this many bands: a warp per band
+#ifndef LSB_FLAT_LOADS
+#define LSB_FLAT_LOADS 4
+#endif
+constexpr int kFlatLoads = LSB_FLAT_LOADS;  // many-band span walk: id loads in flight per lane
 
 template <int NT>
 __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(ProbeArgs a) {
@@ -295,10 +299,11 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(
       }
       band = bl;
     }
-    for (uint32_t pb = p0; pb < p1; pb += 32 * U) {
-      uint32_t idu[U];
+    constexpr int UF = kFlatLoads;  // id loads in flight per lane
+    for (uint32_t pb = p0; pb < p1; pb += 32 * UF) {
+      uint32_t idu[UF];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
+      for (int u = 0; u < UF; ++u) {
         const uint32_t q = pb + 32 * u + lane;
         idu[u] = 0xFFFFFFFFu;
         if (q < p1) {
@@ -308,7 +313,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(
         }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) count_id(idu[u]);
+      for (int u = 0; u < UF; ++u) count_id(idu[u]);
     }
   }
   pdl_trigger();
