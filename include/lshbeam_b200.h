@@ -351,6 +351,12 @@ lsb_status lsb_exact_topb(lsb_ctx* ctx, const lsb_model* model, const float* H, 
  * K4 PARITY issues them); bench.py's roofline denominator for K4. */
 lsb_status lsb_measure_fp32x2_peak(lsb_ctx* ctx, double* lane_ops_per_s);
 
+/* Self-test: out_dev[k] = log((double) p_dev[k]) by the device function the
+ * beam expansion scores with (glibc's log, bit for bit; the reference's
+ * cum + log(p) in src/beam_decoder.cpp is evaluated by the host libm).
+ * Device pointers; synchronises the context stream. */
+lsb_status lsb_selftest_log(lsb_ctx* ctx, const float* p_dev, double* out_dev, size_t n);
+
 /* ---------------------------------- 8. vocabulary-sharded step (cfg 4)
  * One rank's share of a decode step when E is split by contiguous vocabulary
  * slices across ranks (the reference has no multi-device path; SURVEY

@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import glob
+import re
 import os
 import subprocess
 import sys
@@ -44,9 +45,16 @@ def _newer(target: str, deps) -> bool:
     return all(os.path.getmtime(d) <= t for d in deps)
 
 
+def _included_sources(src: str):
+    """The .cu files a source #includes (k_step_fused.cu: the kernel bodies)."""
+    with open(src) as f:
+        names = re.findall(r'^#include "([^"]+\.cu)"', f.read(), re.M)
+    return [os.path.join(os.path.dirname(src), n) for n in names]
+
+
 def _compile(src: str, headers) -> str:
     obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
-    if _newer(obj, [src, *headers, __file__]):
+    if _newer(obj, [src, *headers, *_included_sources(src), __file__]):
         return obj
     cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -60,7 +68,8 @@ def _compile(src: str, headers) -> str:
 def build(verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    headers = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [
+    headers = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + sorted(
+        glob.glob(os.path.join(CSRC, "*.h"))) + [
         os.path.join(ROOT, "include", "lshbeam_b200.h")]
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(lambda s: _compile(s, headers), srcs))

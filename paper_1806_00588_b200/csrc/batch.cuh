@@ -50,6 +50,11 @@ struct lsb_batch {
   uint32_t* seg_count = nullptr;
   lsb::TopEntry* sh_top = nullptr;   // vocabulary-sharded step: local top-B'
   int32_t* sh_topn = nullptr;
+  // small batches: the whole step as one cooperative launch (k_step_fused.cu)
+  int fused = -1;               // -1 undecided, 0 no, 1 yes
+  int fused_grid = 0, fused_rb = 0;
+  uint32_t fused_slice_len = 0;  // probe slices: enough to cover the grid
+  size_t fused_smem = 0;
   // staging for lsb_step_host
   float* h_hidden = nullptr;
   double* h_scores = nullptr;
@@ -98,6 +103,17 @@ namespace lsb {
 // K1+K2 -> K3 -> K4 of one step (profiling events 0..3): candidate sets in
 // b->ids / b->n_cand, logits in b->logits.
 lsb_status step_front(lsb_batch* b, const lsb_state_dev* in, int empty_is_error);
+// The per-kernel arguments of one step on b's scratch (capi_step.cu).
+ProbeArgs probe_args(const lsb_batch* b, const lsb_state_dev* in);
+CompactArgs compact_args(const lsb_batch* b, const lsb_state_dev* in, int empty_is_error);
+LogitsArgs logits_args(const lsb_batch* b, const lsb_state_dev* in);
+SoftmaxArgs softmax_args(const lsb_batch* b, const lsb_state_dev* in);
+ExpandArgs expand_args(const lsb_batch* b, const lsb_state_dev* in, const lsb_out_dev* out);
+// Small batches: the whole lsb_step (K1..K5b) as ONE cooperative launch
+// (k_step_fused.cu). *done = false (and nothing launched) when it does not
+// apply to this batch / step; the caller then runs the separate kernels.
+lsb_status launch_step_fused(lsb_batch* b, const lsb_state_dev* in, const lsb_out_dev* out,
+                             bool* done);
 // Vocabulary-sharded step: phase-2 scratch (capi_shard.cu).
 lsb_status ensure_shard_scratch(lsb_batch* b, int G);
 }  // namespace lsb

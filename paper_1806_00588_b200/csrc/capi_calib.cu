@@ -8,9 +8,16 @@
 // (2 per MAC): the denominator bench.py uses for K4's fp32 roofline, measured
 // on the same GPU in the same run (scripts/micro/fp32x2_tput.cu is the
 // standalone version; 35.2 T lane-ops/s = 121 per SM per clock on B200).
+#include "glibc_log.cuh"
 #include "lsb_internal.cuh"
 
 namespace {
+
+__global__ void k_selftest_log(const float* __restrict__ p, double* __restrict__ out, size_t n) {
+  for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<size_t>(gridDim.x) * blockDim.x)
+    out[k] = lsb::glibc_log(static_cast<double>(p[k]));
+}
 
 constexpr int kCalChains = 16, kCalIters = 2048;
 
@@ -74,5 +81,19 @@ extern "C" lsb_status lsb_measure_fp32x2_peak(lsb_ctx* ctx, double* lane_ops_per
   // 2 FFMA2 per chain step = 2 MACs' FMUL + FADD = 4 lane-ops per thread
   const double lane_ops = static_cast<double>(grid) * 128 * kCalIters * kCalChains * 4;
   *lane_ops_per_s = lane_ops / (best * 1e-3);
+  return LSB_OK;
+}
+
+// Self-test of the device log the beam score uses (glibc_log.cuh): out[k] =
+// log((double) p[k]) for n floats in device memory, on the context stream
+// (synchronised). tests/test_gpu_glibc_log.py compares it with the host libm.
+extern "C" lsb_status lsb_selftest_log(lsb_ctx* ctx, const float* p_dev, double* out_dev,
+                                       size_t n) {
+  if (!ctx || (n && (!p_dev || !out_dev))) return lsb::set_error("lsb_selftest_log: null"), LSB_EINVAL;
+  if (n == 0) return LSB_OK;
+  LSB_CUDA(cudaSetDevice(ctx->device));
+  k_selftest_log<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(p_dev, out_dev, n);
+  LSB_LAUNCHED(ctx, "k_selftest_log");
+  LSB_CUDA(cudaStreamSynchronize(ctx->stream));
   return LSB_OK;
 }

@@ -55,42 +55,26 @@ lsb_status free_batch(lsb_batch* b) {
 
 }  // namespace
 
-lsb_status lsb::step_front(lsb_batch* b, const lsb_state_dev* in, int empty_is_error) {
-  lsb_ctx* ctx = b->ctx;
-  cudaStream_t st = ctx->stream;
-  const int R = b->S * b->B;
-  lsb_status rc;
-  b->rec = b->profile && (b->step_count++ % static_cast<uint64_t>(b->profile_every)) == 0;
-  if (b->rec) {
-    b->ev = &b->ring[static_cast<size_t>(b->ring_next) * 6];
-    b->ring_next = (b->ring_next + 1) % kRing;
-    b->ring_used = std::min(b->ring_used + 1, kRing);
-    LSB_CUDA(cudaEventRecord(b->ev[0], st));
-  }
-  // K1 + K2 (kTopOnly has no index: the bitmap stays empty)
-  if (b->cmode != 2 && b->idx) {
-    ProbeArgs pa{};
-    pa.ix = b->idx->view();
-    pa.hidden = in->hidden;
-    pa.finished = in->finished;
-    pa.n_hyp = in->n_hyp;
-    pa.S = b->S;
-    pa.B = b->B;
-    pa.t = b->t;
-    pa.slice_len = b->slice_len;
-    pa.counter_bytes = b->counter_bytes;
-    pa.levels = b->levels;
-    pa.qcodes = b->qcodes;
-    pa.bitmap = b->bitmap;
-    pa.nwords = b->nwords;
-    pa.err = ctx->err_dev;
-    if ((rc = b->probe_G > 0 ? launch_probe_split(ctx, pa, b->probe_G, b->split_cnt,
-                                                  b->split_words, b->split_arrive)
-                             : launch_probe(ctx, pa)))
-      return rc;
-  }
-  if (b->rec) LSB_CUDA(cudaEventRecord(b->ev[1], st));
-  // K3
+ProbeArgs lsb::probe_args(const lsb_batch* b, const lsb_state_dev* in) {
+  ProbeArgs pa{};
+  pa.ix = b->idx->view();
+  pa.hidden = in->hidden;
+  pa.finished = in->finished;
+  pa.n_hyp = in->n_hyp;
+  pa.S = b->S;
+  pa.B = b->B;
+  pa.t = b->t;
+  pa.slice_len = b->slice_len;
+  pa.counter_bytes = b->counter_bytes;
+  pa.levels = b->levels;
+  pa.qcodes = b->qcodes;
+  pa.bitmap = b->bitmap;
+  pa.nwords = b->nwords;
+  pa.err = b->ctx->err_dev;
+  return pa;
+}
+
+CompactArgs lsb::compact_args(const lsb_batch* b, const lsb_state_dev* in, int empty_is_error) {
   CompactArgs ca{};
   ca.bitmap_in = b->bitmap;
   ca.bitmap_clear = b->bitmap;
@@ -108,14 +92,15 @@ lsb_status lsb::step_front(lsb_batch* b, const lsb_state_dev* in, int empty_is_e
   ca.n_hyp = in->n_hyp;
   ca.finished = in->finished;
   ca.B = b->B;
-  ca.err = ctx->err_dev;
-  if ((rc = launch_compact(ctx, ca, b->S))) return rc;
-  if (b->rec) LSB_CUDA(cudaEventRecord(b->ev[2], st));
-  // K4
+  ca.err = b->ctx->err_dev;
+  return ca;
+}
+
+LogitsArgs lsb::logits_args(const lsb_batch* b, const lsb_state_dev* in) {
   LogitsArgs la{};
   la.H = in->hidden;
   la.d = b->d;
-  la.R_total = R;
+  la.R_total = b->S * b->B;
   la.Bsent = b->B;
   la.E = b->model->E;
   la.bias = b->model->bias;
@@ -129,7 +114,72 @@ lsb_status lsb::step_front(lsb_batch* b, const lsb_state_dev* in, int empty_is_e
   la.tc_A = b->tc_A;
   la.tc_H = b->tc_H;
   la.tc_N = b->tc_N;
-  if ((rc = launch_logits(ctx, la, b->mode, ctx->sm_count * 8))) return rc;
+  return la;
+}
+
+SoftmaxArgs lsb::softmax_args(const lsb_batch* b, const lsb_state_dev* in) {
+  SoftmaxArgs sa{};
+  sa.logits = b->logits;
+  sa.ldl = b->ncap;
+  sa.R_total = b->S * b->B;
+  sa.Bsent = b->B;
+  sa.topB = b->B;
+  sa.n_cand = b->n_cand;
+  sa.finished = in->finished;
+  sa.n_hyp = in->n_hyp;
+  sa.keep_probs = b->keep_probs;
+  sa.top = b->top;
+  sa.top_n = b->top_n;
+  sa.err = b->ctx->err_dev;
+  return sa;
+}
+
+ExpandArgs lsb::expand_args(const lsb_batch* b, const lsb_state_dev* in, const lsb_out_dev* out) {
+  ExpandArgs ea{};
+  ea.S = b->S;
+  ea.Bsent = b->B;
+  ea.topB = b->B;
+  ea.top = b->top;
+  ea.top_n = b->top_n;
+  ea.scores = in->scores;
+  ea.finished = in->finished;
+  ea.n_hyp = in->n_hyp;
+  ea.ids = b->cmode == 0 ? b->ids : nullptr;
+  ea.ncap = b->ncap;
+  ea.n_shared = b->n_shared;
+  ea.hidden = in->hidden;
+  ea.d = b->d;
+  ea.hidden_out = out->hidden_out;
+  ea.choices = out->choices;
+  ea.n_choices = out->n_choices;
+  return ea;
+}
+
+lsb_status lsb::step_front(lsb_batch* b, const lsb_state_dev* in, int empty_is_error) {
+  lsb_ctx* ctx = b->ctx;
+  cudaStream_t st = ctx->stream;
+  lsb_status rc;
+  b->rec = b->profile && (b->step_count++ % static_cast<uint64_t>(b->profile_every)) == 0;
+  if (b->rec) {
+    b->ev = &b->ring[static_cast<size_t>(b->ring_next) * 6];
+    b->ring_next = (b->ring_next + 1) % kRing;
+    b->ring_used = std::min(b->ring_used + 1, kRing);
+    LSB_CUDA(cudaEventRecord(b->ev[0], st));
+  }
+  // K1 + K2 (kTopOnly has no index: the bitmap stays empty)
+  if (b->cmode != 2 && b->idx) {
+    const ProbeArgs pa = probe_args(b, in);
+    if ((rc = b->probe_G > 0 ? launch_probe_split(ctx, pa, b->probe_G, b->split_cnt,
+                                                  b->split_words, b->split_arrive)
+                             : launch_probe(ctx, pa)))
+      return rc;
+  }
+  if (b->rec) LSB_CUDA(cudaEventRecord(b->ev[1], st));
+  // K3
+  if ((rc = launch_compact(ctx, compact_args(b, in, empty_is_error), b->S))) return rc;
+  if (b->rec) LSB_CUDA(cudaEventRecord(b->ev[2], st));
+  // K4
+  if ((rc = launch_logits(ctx, logits_args(b, in), b->mode, ctx->sm_count * 8))) return rc;
   if (b->rec) LSB_CUDA(cudaEventRecord(b->ev[3], st));
   return LSB_OK;
 }
@@ -340,40 +390,20 @@ lsb_status lsb_step(lsb_batch* b, const lsb_state_dev* in, const lsb_out_dev* ou
     return set_error("lsb_step: null argument"), LSB_EINVAL;
   lsb_ctx* ctx = b->ctx;
   cudaStream_t st = ctx->stream;
-  const int R = b->S * b->B;
-  lsb_status rc = step_front(b, in, 1);
+  // small batches: the whole step in one cooperative launch (k_step_fused.cu)
+  bool fused = false;
+  lsb_status rc = launch_step_fused(b, in, out, &fused);
+  if (rc) return rc;
+  if (fused) {
+    b->last = *in;
+    b->has_last = true;
+    return LSB_OK;
+  }
+  rc = step_front(b, in, 1);
   if (rc) return rc;
   // K5a + K5b
-  SoftmaxArgs sa{};
-  sa.logits = b->logits;
-  sa.ldl = b->ncap;
-  sa.R_total = R;
-  sa.Bsent = b->B;
-  sa.topB = b->B;
-  sa.n_cand = b->n_cand;
-  sa.finished = in->finished;
-  sa.n_hyp = in->n_hyp;
-  sa.keep_probs = b->keep_probs;
-  sa.top = b->top;
-  sa.top_n = b->top_n;
-  sa.err = ctx->err_dev;
-  ExpandArgs ea{};
-  ea.S = b->S;
-  ea.Bsent = b->B;
-  ea.topB = b->B;
-  ea.top = b->top;
-  ea.top_n = b->top_n;
-  ea.scores = in->scores;
-  ea.finished = in->finished;
-  ea.n_hyp = in->n_hyp;
-  ea.ids = b->cmode == 0 ? b->ids : nullptr;
-  ea.ncap = b->ncap;
-  ea.n_shared = b->n_shared;
-  ea.hidden = in->hidden;
-  ea.d = b->d;
-  ea.hidden_out = out->hidden_out;
-  ea.choices = out->choices;
-  ea.n_choices = out->n_choices;
+  const SoftmaxArgs sa = softmax_args(b, in);
+  const ExpandArgs ea = expand_args(b, in, out);
   // K5 variant (LSB_K5): 0 = CTA-per-row softmax + per-sentence expansion
   // (default; measured fastest with the K5b reorder batched), 1 = warp-per-row
   // softmax + expansion, 2 = one fused launch per sentence. All three are

@@ -155,13 +155,16 @@ __device__ __forceinline__ void mac4_x2(unsigned long long (&acc)[RB][CB][2], co
 // lanes of a row group and its E loads by the 4 of a column group, so one
 // 16-byte LDS is a single wavefront (vs 4 for 32 distinct E rows) and a
 // thread issues RB/4 + TC loads per 4-step instead of RB + 1.
+// One K4 job (a shared-block tile or a sentence row group's survivor tiles)
+// by a 128-thread CTA; `bid` is the job index. k_logits runs a CTA per job;
+// the fused small-batch step (k_step_fused.cu) loops its persistent CTAs over
+// the jobs.
 template <int RB, int CB, bool PARITY, bool VEC, int kStages, int KC, bool TWO_D = false>
-__global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs a) {
+__device__ __forceinline__ void logits_job(const LogitsArgs& a, int bid, float* sm) {
   constexpr int kKC = KC;
   constexpr int kKS = KC + 4;
   constexpr int kParts = KC / 4;           // 16-byte pieces per row chunk
   constexpr int kRowStep = kLT / kParts;   // rows covered by one pass of the CTA
-  extern __shared__ __align__(16) float sm[];
   constexpr int CT = tile_cols<CB, TWO_D>();
   constexpr int STAGE = (CT + RB) * kKS;
   constexpr int NA = PARITY ? 4 : 1;
@@ -178,19 +181,18 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
   const int d4 = d & ~3;
   const int nchunks = (d + kKC - 1) / kKC;
 
-  pdl_wait();
-  const bool shared_job = static_cast<int>(blockIdx.x) < a.jobs_shared;
+  const bool shared_job = bid < a.jobs_shared;
   int row0, rowlim, tile_first, tile_step, s = 0;
   uint32_t m = 0;
   if (shared_job) {
-    const int rg = blockIdx.x / a.ctiles_shared;
+    const int rg = bid / a.ctiles_shared;
     row0 = rg * RB;
     rowlim = a.R_total;
-    tile_first = blockIdx.x % a.ctiles_shared;
+    tile_first = bid % a.ctiles_shared;
     tile_step = a.ctiles_shared;  // exactly one tile
     m = a.n_shared;
   } else {
-    const int e = blockIdx.x - a.jobs_shared;
+    const int e = bid - a.jobs_shared;
     s = e / (a.G * a.X);
     const int g = (e / a.X) % a.G;
     row0 = s * a.Bsent + g * RB;
@@ -208,7 +210,7 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
     const uint32_t col0 = (shared_job ? 0u : a.n_shared) + t0;
     __syncthreads();  // previous tile's readers are done with sid / stages
     for (int c = tid; c < CT; c += kLT)
-      sid[c] = c < ncols ? (list ? __ldg(list + t0 + c) : t0 + c) : 0u;
+      sid[c] = c < ncols ? (list ? __ldcg(list + t0 + c) : t0 + c) : 0u;  // (cg: K3 may have written it in the same fused launch)
     __syncthreads();
 
     // per-tile source offsets (elements) of this thread's 16-byte pieces:
@@ -400,6 +402,14 @@ __global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs
       }
     }
   }
+}
+
+#ifndef LSB_BODIES_ONLY  // (k_step_fused.cu includes this file for logits_job)
+template <int RB, int CB, bool PARITY, bool VEC, int kStages, int KC, bool TWO_D = false>
+__global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs a) {
+  extern __shared__ __align__(16) float sm[];
+  pdl_wait();
+  logits_job<RB, CB, PARITY, VEC, kStages, KC, TWO_D>(a, blockIdx.x, sm);
 }
 
 // Rows per CTA for beam B: minimise the padded rows a sentence costs,
@@ -601,5 +611,7 @@ static lsb_status launch_logits_survivors(lsb_ctx* ctx, LogitsArgs a, lsb_mode m
 #undef LSB_RB
 #undef LSB_RB2
 }
+
+#endif  // LSB_BODIES_ONLY
 
 }  // namespace lsb

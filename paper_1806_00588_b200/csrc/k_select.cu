@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cfloat>
 
+#include "glibc_log.cuh"
 #include "k_step.cuh"
 
 namespace lsb {
@@ -55,8 +56,14 @@ struct FMaxOp {
 struct DSumOp {
   __device__ double operator()(double x, double y) const { return x + y; }
 };
-__device__ constexpr FMaxOp fmax_op{};
-__device__ constexpr DSumOp dsum_op{};
+// log((double) p) of a row probability as the reference's host libm
+// computes it (glibc_log.cuh: bit for bit; CUDA's log() is within 1 ulp and
+// differed on one score of a test step); the score is then
+// __dadd_rn(cum, log_p(p)), never contracted.
+static __device__ __forceinline__ double log_p(float p) { return glibc_log(static_cast<double>(p)); }
+
+static __device__ constexpr FMaxOp fmax_op{};
+static __device__ constexpr DSumOp dsum_op{};
 
 // The K-th largest of the CTA's kSelT per-thread values x (-1 = none): each
 // warp sorts its 32 with a shuffle bitonic network, every lane ranks its value
@@ -257,15 +264,15 @@ __device__ __forceinline__ void row_registers(const SoftmaxArgs& a, int row, flo
 }
 
 // ===================================================================== K5a
-__global__ void __launch_bounds__(kSelT) k_softmax_topb(SoftmaxArgs a) {
+// One row's softmax + top-B by a 128-thread CTA (k_softmax_topb: a CTA per
+// row; the fused small-batch step calls it from persistent CTAs).
+static __device__ void softmax_row(const SoftmaxArgs& a, int row) {
   __shared__ float red_f[kSelT / 32];
   __shared__ double red_d[kSelT / 32];
   __shared__ float win_p[kSelT / 32];
   __shared__ uint32_t win_r[kSelT / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int row = blockIdx.x;
   const int s = row / a.Bsent, i = row % a.Bsent;
-  pdl_wait();
   const bool live = !(a.n_hyp && i >= a.n_hyp[s]) && !(a.finished && a.finished[row]);
   if (!live) {
     if (tid == 0) a.top_n[row] = 0;
@@ -413,12 +420,19 @@ __global__ void __launch_bounds__(kSelT) k_softmax_topb(SoftmaxArgs a) {
   if (tid == 0) a.top_n[row] = keep;
 }
 
+#ifndef LSB_BODIES_ONLY  // (k_step_fused.cu includes this file for its device functions)
+__global__ void __launch_bounds__(kSelT) k_softmax_topb(SoftmaxArgs a) {
+  pdl_wait();
+  softmax_row(a, blockIdx.x);
+}
+
 lsb_status launch_softmax(lsb_ctx* ctx, const SoftmaxArgs& a) {
   if (a.R_total == 0) return LSB_OK;
   LSB_CUDA(launch_pdl(ctx, k_softmax_topb, dim3(a.R_total), dim3(kSelT), 0, a));
   LSB_LAUNCHED(ctx, "k_softmax_topb");
   return LSB_OK;
 }
+#endif  // LSB_BODIES_ONLY
 
 // ===================================================================== K5b
 struct Cand {
@@ -444,7 +458,7 @@ __device__ __forceinline__ long long word_of(const ExpandArgs& a, const uint32_t
 // One flat (child, float4) index space; each thread keeps 8 loads in flight
 // before storing (a load->store chain per element would serialise on
 // latency: the store could alias the next load).
-__device__ void reorder_hidden(const ExpandArgs& a, int s, int count, const uint32_t* beams) {
+static __device__ void reorder_hidden(const ExpandArgs& a, int s, int count, const uint32_t* beams) {
   const int d = a.d;
   const size_t rbase = static_cast<size_t>(s) * a.Bsent;
   const size_t obase = static_cast<size_t>(s) * a.topB;
@@ -500,14 +514,12 @@ __device__ void reorder_hidden(const ExpandArgs& a, int s, int count, const uint
 // Shared memory: per list off/len (ints), then per candidate score, beam, word.
 constexpr int kRankMaxLists = 128;
 
-template <int NT>
-__global__ void __launch_bounds__(NT) k_expand(ExpandArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
+// One sentence's expansion by the whole CTA (any blockDim); smem holds the
+// candidates (expand_smem_bytes). k_expand runs a CTA per sentence.
+static __device__ void expand_sentence(const ExpandArgs& a, int s, unsigned char* smem) {
   __shared__ int s_off[kRankMaxLists + 1];
   __shared__ uint32_t s_beams[64];
   __shared__ int s_count;
-  pdl_wait();
-  const int s = blockIdx.x;
   const int R = a.Bsent;
   const int nfz = a.frozen_mode ? a.nfrozen : 0;
   const int nl = nfz + R;
@@ -575,7 +587,7 @@ __global__ void __launch_bounds__(NT) k_expand(ExpandArgs a) {
         wd = -1;
       } else {
         const TopEntry t = a.top[(rbase + row) * a.topB + j];
-        sc = a.scores[rbase + row] + log(static_cast<double>(t.p));
+        sc = __dadd_rn(a.scores[rbase + row], log_p(t.p));
         wd = word_of(a, ids, t.r);
       }
     }
@@ -665,6 +677,19 @@ __global__ void __launch_bounds__(NT) k_expand(ExpandArgs a) {
   if (a.hidden_out && a.hidden) reorder_hidden(a, s, min(s_count, 64), s_beams);
 }
 
+#ifndef LSB_BODIES_ONLY
+template <int NT>
+__global__ void __launch_bounds__(NT) k_expand(ExpandArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  pdl_wait();
+  expand_sentence(a, blockIdx.x, smem);
+}
+
+size_t expand_smem_bytes(const ExpandArgs& a) {
+  const int nl = (a.frozen_mode ? a.nfrozen : 0) + a.Bsent;
+  return static_cast<size_t>(nl) * std::max(a.topB, 1) * (8 + 8 + 4 + 4 + 4 + 4);
+}
+
 // B-round warp tournament over list heads (any number of lists).
 __global__ void k_expand_tournament(ExpandArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -685,7 +710,7 @@ __global__ void k_expand_tournament(ExpandArgs a) {
   const uint32_t* ids = a.ids ? a.ids + static_cast<size_t>(s) * a.ncap : nullptr;
   auto live_score = [&](int row, int pos, double& sc, long long& wd) {
     const TopEntry e = a.top[(rbase + row) * a.topB + pos];
-    sc = a.scores[rbase + row] + log(static_cast<double>(e.p));
+    sc = __dadd_rn(a.scores[rbase + row], log_p(e.p));
     wd = word_of(a, ids, e.r);
   };
   if (threadIdx.x < 32) {
@@ -987,7 +1012,7 @@ __global__ void __launch_bounds__(kFusedMaxB * 32) k_select_fused(SoftmaxArgs sa
       wd = -1;
     } else {
       const TopEntry t = ea.top[(rbase + l) * B + j];
-      sc = ea.scores[rbase + l] + log(static_cast<double>(t.p));
+      sc = __dadd_rn(ea.scores[rbase + l], log_p(t.p));
       wd = word_of(ea, ids, t.r);
     }
     s_score[e] = sc;
@@ -1094,5 +1119,7 @@ lsb_status launch_expand(lsb_ctx* ctx, const ExpandArgs& a) {
   LSB_LAUNCHED(ctx, "k_expand_tournament");
   return LSB_OK;
 }
+
+#endif  // LSB_BODIES_ONLY
 
 }  // namespace lsb

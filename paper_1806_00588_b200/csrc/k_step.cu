@@ -20,6 +20,141 @@
 
 namespace lsb {
 
+// ====================================================================== K3
+__device__ __forceinline__ uint32_t below_mask(uint32_t word, uint32_t T) {
+  // bits of ids < T inside bitmap word `word`
+  const uint32_t base = word * 32;
+  if (T >= base + 32) return 0xFFFFFFFFu;
+  if (T <= base) return 0u;
+  return (1u << (T - base)) - 1u;
+}
+
+__device__ __forceinline__ uint32_t valid_mask(uint32_t word, uint32_t V) {
+  return below_mask(word, V);
+}
+
+static __device__ uint32_t block_scan_excl(uint32_t v, uint32_t* wsum, uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarp = (blockDim.x + 31) >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t z = lane < nwarp ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    if (lane < nwarp) wsum[lane] = z;
+    if (lane == 31) wsum[32] = z;
+  }
+  __syncthreads();
+  const uint32_t r = (warp ? wsum[warp - 1] : 0) + x - v;
+  if (total) *total = wsum[32];
+  __syncthreads();
+  return r;
+}
+
+// One sentence's K3 by the whole CTA (any blockDim <= 1024): bm = nwords
+// words of shared memory. k_compact runs a CTA per sentence; the fused
+// small-batch step (k_step_fused.cu) calls it from a persistent CTA.
+static __device__ void compact_sentence(const CompactArgs& a, int s, uint32_t* bm) {
+  __shared__ uint32_t wsum[33];
+  __shared__ uint32_t s_thr, s_below, s_spec;
+  uint32_t* ids = a.ids + static_cast<size_t>(s) * a.ncap;
+  if (a.mode != 0) {
+    // t == 0 (every word survives, src/candidate_selector.cpp:21-27) or
+    // full vocabulary: the candidate list is the identity; ids are implicit.
+    if (threadIdx.x == 0) {
+      a.n_cand[s] = a.V;
+      a.prov[3 * s] = a.mode == 1 ? a.V : 0;
+      a.prov[3 * s + 1] = 0;
+      a.prov[3 * s + 2] = 0;
+    }
+    return;
+  }
+  const uint32_t nw = a.nwords;
+  if (threadIdx.x == 0) {
+    s_thr = 0;
+    s_below = 0;
+    s_spec = 0;
+  }
+  uint32_t thr = 0, below = 0;
+  for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) {
+    // L2 read: in the fused step the bits were set by other CTAs' atomics
+    uint32_t m = a.bitmap_in ? __ldcg(a.bitmap_in + static_cast<size_t>(s) * nw + w) : 0u;
+    if (a.bitmap_clear) a.bitmap_clear[static_cast<size_t>(s) * nw + w] = 0u;
+    m &= valid_mask(w, a.V);
+    bm[w] = m;
+    thr += __popc(m);
+    below += __popc(m & below_mask(w, a.T));
+  }
+  __syncthreads();
+  atomicAdd(&s_thr, thr);
+  atomicAdd(&s_below, below);
+  // specials >= T that are not threshold survivors are new
+  // (src/candidate_selector.cpp:85-101); specials < T are inside [0,T).
+  for (int k = threadIdx.x; k < a.nspec; k += blockDim.x) {
+    const uint32_t id = a.specials[k];
+    if (id >= a.T) {
+      const uint32_t bit = 1u << (id & 31);
+      const uint32_t old = atomicOr(&bm[id >> 5], bit);
+      if (!(old & bit)) atomicAdd(&s_spec, 1u);
+    }
+  }
+  __syncthreads();
+  // Every id < T is a candidate (the top-T merge), so positions [0, T) hold
+  // 0..T-1 -- written coalesced by all threads -- and an id >= T sits at
+  // T + its rank among the set bits >= T: per-thread contiguous word ranges,
+  // one block scan, ordered emit of the (few) bits above the prefix.
+  pdl_trigger();
+  for (uint32_t i = threadIdx.x; i < a.T; i += blockDim.x) ids[i] = i;
+  const uint32_t per = (nw + blockDim.x - 1) / blockDim.x;
+  const uint32_t w0 = threadIdx.x * per, w1 = min(nw, w0 + per);
+  uint32_t cnt = 0;
+  for (uint32_t w = w0; w < w1; ++w) cnt += __popc(bm[w] & ~below_mask(w, a.T));
+  uint32_t total;
+  uint32_t base = a.T + block_scan_excl(cnt, wsum, &total);
+  total += a.T;
+  for (uint32_t w = w0; w < w1; ++w) {
+    uint32_t m = bm[w] & ~below_mask(w, a.T);
+    while (m) {
+      const int b = __ffs(m) - 1;
+      ids[base++] = w * 32 + b;
+      m &= m - 1;
+    }
+  }
+  if (threadIdx.x == 0) {
+    a.n_cand[s] = total;
+    a.prov[3 * s] = s_thr;
+    a.prov[3 * s + 1] = a.T - s_below;
+    a.prov[3 * s + 2] = s_spec;
+    if (total == 0 && a.empty_is_error) {
+      bool live = true;
+      if (a.n_hyp) {
+        live = false;
+        for (int i = 0; i < a.n_hyp[s]; ++i)
+          live |= !(a.finished && a.finished[static_cast<size_t>(s) * a.B + i]);
+      }
+      if (live) atomicOr(a.err, kErrEmptyCands);
+    }
+  }
+}
+
+#ifndef LSB_BODIES_ONLY  // (k_step_fused.cu includes this file for its device functions)
+__global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
+  extern __shared__ uint32_t bm_dyn[];  // nwords
+  pdl_wait();
+  compact_sentence(a, blockIdx.x, bm_dyn);
+}
+#endif
+
 // =================================================================== K1+K2
 constexpr int kWarpBands = 64;  // up to this many bands: a warp per band
 #ifndef LSB_FLAT_LOADS
@@ -27,14 +162,13 @@ constexpr int kWarpBands = 64;  // up to this many bands: a warp per band
 #endif
 constexpr int kFlatLoads = LSB_FLAT_LOADS;  // many-band span walk: id loads in flight per lane
 
-template <int NT>
-__global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(ProbeArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
+// One CTA's K1+K2 for hypothesis row `row` and vocabulary slice `slice`
+// (any blockDim <= 1024); returns uniformly per CTA.
+static __device__ void probe_row(const ProbeArgs& a, unsigned char* smem, int row, int slice) {
   const IndexView& ix = a.ix;
-  const int row = blockIdx.x;
   const int s = row / a.B, i = row % a.B;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  const uint32_t lo = blockIdx.y * a.slice_len;
+  const uint32_t lo = static_cast<uint32_t>(slice) * a.slice_len;
   const uint32_t hi = min(ix.V, lo + a.slice_len);
   const bool count = a.t > 0;
   const bool bits = a.levels >= 0;  // bit-sliced counting (t <= 8)
@@ -161,7 +295,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(
     uint32_t code = 0;
     for (int b = 0; b < ix.u; ++b) code |= static_cast<uint32_t>(idx[w * ix.u + b]) << (b * ix.bits);
     codes[w] = code;
-    if (blockIdx.y == 0) a.qcodes[static_cast<size_t>(row) * ix.W + w] = code;
+    if (slice == 0) a.qcodes[static_cast<size_t>(row) * ix.W + w] = code;
   }
   __syncthreads();
   if (!count) return;
@@ -325,6 +459,22 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(
     for (uint32_t w = threadIdx.x; w < wend; w += blockDim.x)
       if (fin[w]) atomicOr(bm + w0 + w, fin[w]);
   }
+}
+
+#ifndef LSB_BODIES_ONLY
+template <int NT>
+__global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(ProbeArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  probe_row(a, smem, blockIdx.x, blockIdx.y);
+}
+
+size_t probe_smem_bytes(const ProbeArgs& a) {
+  const IndexView& ix = a.ix;
+  const size_t cbytes =
+      a.t <= 0 ? 0
+      : a.levels >= 0 ? static_cast<size_t>(a.levels + 1) * (a.slice_len / 8)
+                      : ((static_cast<size_t>(a.slice_len) * a.counter_bytes + 15) & ~size_t(15));
+  return cbytes + ((ix.d + 3) & ~3) * 4 + (3 * ix.W + 1) * 4 + 2 * ix.P + 16;
 }
 
 lsb_status launch_probe(lsb_ctx* ctx, const ProbeArgs& a) {
@@ -517,132 +667,6 @@ lsb_status launch_probe_split(lsb_ctx* ctx, const ProbeArgs& a, int G, uint32_t*
   return LSB_OK;
 }
 
-// ====================================================================== K3
-__device__ __forceinline__ uint32_t below_mask(uint32_t word, uint32_t T) {
-  // bits of ids < T inside bitmap word `word`
-  const uint32_t base = word * 32;
-  if (T >= base + 32) return 0xFFFFFFFFu;
-  if (T <= base) return 0u;
-  return (1u << (T - base)) - 1u;
-}
-
-__device__ __forceinline__ uint32_t valid_mask(uint32_t word, uint32_t V) {
-  return below_mask(word, V);
-}
-
-__device__ uint32_t block_scan_excl(uint32_t v, uint32_t* wsum, uint32_t* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nwarp = (blockDim.x + 31) >> 5;
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) wsum[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t z = lane < nwarp ? wsum[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
-      if (lane >= o) z += y;
-    }
-    if (lane < nwarp) wsum[lane] = z;
-    if (lane == 31) wsum[32] = z;
-  }
-  __syncthreads();
-  const uint32_t r = (warp ? wsum[warp - 1] : 0) + x - v;
-  if (total) *total = wsum[32];
-  __syncthreads();
-  return r;
-}
-
-__global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
-  extern __shared__ uint32_t bm[];  // nwords
-  __shared__ uint32_t wsum[33];
-  __shared__ uint32_t s_thr, s_below, s_spec;
-  const int s = blockIdx.x;
-  pdl_wait();
-  uint32_t* ids = a.ids + static_cast<size_t>(s) * a.ncap;
-  if (a.mode != 0) {
-    // t == 0 (every word survives, src/candidate_selector.cpp:21-27) or
-    // full vocabulary: the candidate list is the identity; ids are implicit.
-    if (threadIdx.x == 0) {
-      a.n_cand[s] = a.V;
-      a.prov[3 * s] = a.mode == 1 ? a.V : 0;
-      a.prov[3 * s + 1] = 0;
-      a.prov[3 * s + 2] = 0;
-    }
-    return;
-  }
-  const uint32_t nw = a.nwords;
-  if (threadIdx.x == 0) {
-    s_thr = 0;
-    s_below = 0;
-    s_spec = 0;
-  }
-  uint32_t thr = 0, below = 0;
-  for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) {
-    uint32_t m = a.bitmap_in ? a.bitmap_in[static_cast<size_t>(s) * nw + w] : 0u;
-    if (a.bitmap_clear) a.bitmap_clear[static_cast<size_t>(s) * nw + w] = 0u;
-    m &= valid_mask(w, a.V);
-    bm[w] = m;
-    thr += __popc(m);
-    below += __popc(m & below_mask(w, a.T));
-  }
-  __syncthreads();
-  atomicAdd(&s_thr, thr);
-  atomicAdd(&s_below, below);
-  // specials >= T that are not threshold survivors are new
-  // (src/candidate_selector.cpp:85-101); specials < T are inside [0,T).
-  for (int k = threadIdx.x; k < a.nspec; k += blockDim.x) {
-    const uint32_t id = a.specials[k];
-    if (id >= a.T) {
-      const uint32_t bit = 1u << (id & 31);
-      const uint32_t old = atomicOr(&bm[id >> 5], bit);
-      if (!(old & bit)) atomicAdd(&s_spec, 1u);
-    }
-  }
-  __syncthreads();
-  // Every id < T is a candidate (the top-T merge), so positions [0, T) hold
-  // 0..T-1 -- written coalesced by all threads -- and an id >= T sits at
-  // T + its rank among the set bits >= T: per-thread contiguous word ranges,
-  // one block scan, ordered emit of the (few) bits above the prefix.
-  pdl_trigger();
-  for (uint32_t i = threadIdx.x; i < a.T; i += blockDim.x) ids[i] = i;
-  const uint32_t per = (nw + blockDim.x - 1) / blockDim.x;
-  const uint32_t w0 = threadIdx.x * per, w1 = min(nw, w0 + per);
-  uint32_t cnt = 0;
-  for (uint32_t w = w0; w < w1; ++w) cnt += __popc(bm[w] & ~below_mask(w, a.T));
-  uint32_t total;
-  uint32_t base = a.T + block_scan_excl(cnt, wsum, &total);
-  total += a.T;
-  for (uint32_t w = w0; w < w1; ++w) {
-    uint32_t m = bm[w] & ~below_mask(w, a.T);
-    while (m) {
-      const int b = __ffs(m) - 1;
-      ids[base++] = w * 32 + b;
-      m &= m - 1;
-    }
-  }
-  if (threadIdx.x == 0) {
-    a.n_cand[s] = total;
-    a.prov[3 * s] = s_thr;
-    a.prov[3 * s + 1] = a.T - s_below;
-    a.prov[3 * s + 2] = s_spec;
-    if (total == 0 && a.empty_is_error) {
-      bool live = true;
-      if (a.n_hyp) {
-        live = false;
-        for (int i = 0; i < a.n_hyp[s]; ++i)
-          live |= !(a.finished && a.finished[static_cast<size_t>(s) * a.B + i]);
-      }
-      if (live) atomicOr(a.err, kErrEmptyCands);
-    }
-  }
-}
-
 lsb_status launch_compact(lsb_ctx* ctx, const CompactArgs& a, int S) {
   const size_t smem = static_cast<size_t>(a.nwords) * 4;
   if (smem > ctx->smem_optin) return set_error("compact: vocabulary too large"), LSB_EINVAL;
@@ -701,5 +725,7 @@ lsb_status launch_gather(lsb_ctx* ctx, const float* E, int d, const uint32_t* id
   LSB_LAUNCHED(ctx, "k_gather");
   return LSB_OK;
 }
+
+#endif  // LSB_BODIES_ONLY
 
 }  // namespace lsb

@@ -109,6 +109,8 @@ struct ExpandArgs {
 };
 
 lsb_status launch_probe(lsb_ctx* ctx, const ProbeArgs& a);
+// dynamic shared memory of one probe_row CTA (k_probe_count)
+size_t probe_smem_bytes(const ProbeArgs& a);
 // Band-split K1+K2 for few rows (k_step.cu): grid (rows, G band groups),
 // 16-bit hit counters cnt[rows][cnt_words] in global memory, zero on entry
 // and left zero (self-cleaning), arrive[rows] zero likewise.
@@ -148,6 +150,8 @@ struct SegArgs {
 int seg_count(lsb_ctx* ctx, int R, uint32_t n, int B);
 lsb_status launch_softmax_seg(lsb_ctx* ctx, const SegArgs& g);
 lsb_status launch_expand(lsb_ctx* ctx, const ExpandArgs& a);
+// dynamic shared memory of one expand_sentence CTA (rank path)
+size_t expand_smem_bytes(const ExpandArgs& a);
 // Fused K5a+K5b (one launch; see k_select.cu) when select_fused_applies().
 bool select_fused_applies(const SoftmaxArgs& sa, const ExpandArgs& ea);
 // K5a with one warp per row (rows <= 32*48 candidates in registers).

@@ -80,6 +80,11 @@ class Context:
         N.check(self.lib.lsb_measure_fp32x2_peak(self.h, C.byref(v)), "lsb_measure_fp32x2_peak")
         return float(v.value)
 
+    def selftest_log(self, p_dev: int, out_dev: int, n: int):
+        """out[k] = log((double) p[k]) by the device's glibc-exact log
+        (lsb_selftest_log); device pointers."""
+        N.check(self.lib.lsb_selftest_log(self.h, p_dev, out_dev, n), "lsb_selftest_log")
+
     @property
     def launches(self) -> int:
         return int(self.lib.lsb_ctx_launch_count(self.h))

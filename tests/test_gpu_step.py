@@ -101,6 +101,69 @@ def test_step_matches_oracle(ctx, oracle, V, d, K, u, W, S, B, T, t, frozen):
             np.testing.assert_array_equal(hout[s, k], hidden[s, beam])
 
 
+# The opt-in single-launch step for small batches (k_step_fused.cu,
+# LSB_FUSED=1): the same device functions as the separate kernels in one
+# cooperative launch, with the probe split into more vocabulary slices.
+FUSED_CASES = [
+    # V, d, K, u, W, S, B, T, t
+    (4000, 64, 8, 3, 16, 4, 12, 100, 2),
+    (4000, 64, 8, 3, 16, 3, 12, 0, 1),
+    (4000, 64, 4, 2, 8, 2, 8, 100, 1),
+    (8000, 64, 8, 3, 16, 2, 12, 4000, 2),
+    (6000, 100, 16, 3, 24, 1, 12, 50, 12),  # t > 8: byte counters
+]
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("V,d,K,u,W,S,B,T,t", FUSED_CASES)
+@pytest.mark.parametrize("frozen", [False, True])
+def test_fused_small_step_matches_oracle(ctx, oracle, monkeypatch, mode, V, d, K, u, W, S, B, T,
+                                         t, frozen):
+    from paper_1806_00588_b200 import Batch, Index, Model
+    monkeypatch.setenv("LSB_FUSED", "1")
+    E, bias, perms, bt, ps, isd = make_world(oracle, V, d, K, u, W, seed=V + d,
+                                             bias_strength=8.0)
+    specials = [V - 1]
+    state = make_state(oracle, S, B, d, seed=V * 3 + d, frozen_every=3 if frozen else 0,
+                       short=(B // 2 if frozen else 0))
+    m = Model(ctx, E, bias)
+    idx = Index(ctx, m, K=K, u=u, W=W, perm_seed=ps, index_seed=isd)
+    b = Batch(ctx, m, idx, S=S, B=B, T=T, t=t, specials=specials, mode=mode)
+    b.keep_probs(True)
+    hidden, scores, finished, n_hyp = state
+    n0 = ctx.launches
+    res, hout = b.step_host(hidden, scores, finished, n_hyp, want_hidden=True)
+    assert ctx.launches - n0 == 1  # the whole step is one launch
+    for s in range(S):
+        want = oracle_step(oracle, bt, perms, E, bias, K, u, W, hidden[s], scores[s],
+                           finished[s], int(n_hyp[s]), B, T, t, specials)
+        ids, prov = b.candidates(s)
+        np.testing.assert_array_equal(ids, want["ids"])
+        assert prov == want["prov"]
+        np.testing.assert_array_equal(b.query_codes(s, W)[want["live"]], want["codes"])
+        if mode == 0:
+            np.testing.assert_array_equal(b.probs(s).view(np.uint32),
+                                          want["probs"].view(np.uint32))
+        ws, wb, ww = want["choices"]
+        if mode == 0:
+            assert [c[2] for c in res[s]] == ww.tolist()
+            assert [c[1] for c in res[s]] == wb.tolist()
+            np.testing.assert_array_equal(np.array([c[0] for c in res[s]]), ws)
+        for k, (_, beam, _) in enumerate(res[s]):
+            np.testing.assert_array_equal(hout[s, k], hidden[s, beam])
+    # and bit-for-bit the separate kernels' step (FAST included)
+    monkeypatch.setenv("LSB_FUSED", "0")
+    b2 = Batch(ctx, m, idx, S=S, B=B, T=T, t=t, specials=specials, mode=mode)
+    b2.keep_probs(True)
+    res2, hout2 = b2.step_host(hidden, scores, finished, n_hyp, want_hidden=True)
+    assert res2 == res
+    np.testing.assert_array_equal(hout2.view(np.uint32), hout.view(np.uint32))
+    for s in range(S):
+        np.testing.assert_array_equal(b2.probs(s).view(np.uint32), b.probs(s).view(np.uint32))
+    b.close()
+    b2.close()
+
+
 def test_step_config1_shape(ctx, oracle):
     """BASELINE config 1 shapes: V=40k, d=1000, B=12, K=8, u=3, W=16, T=1000, t=2."""
     V, d, K, u, W, B, T, t, S = 40000, 1000, 8, 3, 16, 12, 1000, 2, 2
