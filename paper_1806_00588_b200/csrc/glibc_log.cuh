@@ -13,7 +13,7 @@ namespace glibc_log_detail {
 #undef LSB_LOG_CONST
 }  // namespace glibc_log_detail
 
-#define LSB_LOG_FN static __device__ __noinline__ double glibc_log(double x)
+#define LSB_LOG_FN static __device__ __forceinline__ double glibc_log(double x)
 #define LSB_FMA(a, b, c) __fma_rn((a), (b), (c))
 #define LSB_MUL(a, b) __dmul_rn((a), (b))
 #define LSB_ADD(a, b) __dadd_rn((a), (b))

@@ -159,6 +159,13 @@ __device__ __forceinline__ void mac4_x2(unsigned long long (&acc)[RB][CB][2], co
 // by a 128-thread CTA; `bid` is the job index. k_logits runs a CTA per job;
 // the fused small-batch step (k_step_fused.cu) loops its persistent CTAs over
 // the jobs.
+// Survivor ids: read-only for k_logits; written by K3 in the same launch in
+// the fused step (k_step_fused.cu), which must not use the read-only path.
+#ifdef LSB_BODIES_ONLY
+#define LSB_LD_IDS(p) __ldcg(p)
+#else
+#define LSB_LD_IDS(p) __ldg(p)
+#endif
 template <int RB, int CB, bool PARITY, bool VEC, int kStages, int KC, bool TWO_D = false>
 __device__ __forceinline__ void logits_job(const LogitsArgs& a, int bid, float* sm) {
   constexpr int kKC = KC;
@@ -181,6 +188,7 @@ __device__ __forceinline__ void logits_job(const LogitsArgs& a, int bid, float* 
   const int d4 = d & ~3;
   const int nchunks = (d + kKC - 1) / kKC;
 
+  pdl_wait();  // (no-op unless launched as a PDL dependent)
   const bool shared_job = bid < a.jobs_shared;
   int row0, rowlim, tile_first, tile_step, s = 0;
   uint32_t m = 0;
@@ -210,7 +218,7 @@ __device__ __forceinline__ void logits_job(const LogitsArgs& a, int bid, float* 
     const uint32_t col0 = (shared_job ? 0u : a.n_shared) + t0;
     __syncthreads();  // previous tile's readers are done with sid / stages
     for (int c = tid; c < CT; c += kLT)
-      sid[c] = c < ncols ? (list ? __ldcg(list + t0 + c) : t0 + c) : 0u;  // (cg: K3 may have written it in the same fused launch)
+      sid[c] = c < ncols ? (list ? LSB_LD_IDS(list + t0 + c) : t0 + c) : 0u;
     __syncthreads();
 
     // per-tile source offsets (elements) of this thread's 16-byte pieces:
@@ -406,9 +414,8 @@ __device__ __forceinline__ void logits_job(const LogitsArgs& a, int bid, float* 
 
 #ifndef LSB_BODIES_ONLY  // (k_step_fused.cu includes this file for logits_job)
 template <int RB, int CB, bool PARITY, bool VEC, int kStages, int KC, bool TWO_D = false>
-__global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(LogitsArgs a) {
+__global__ void __launch_bounds__(kLT, kStages == 2 ? 5 : 3) k_logits(const __grid_constant__ LogitsArgs a) {
   extern __shared__ __align__(16) float sm[];
-  pdl_wait();
   logits_job<RB, CB, PARITY, VEC, kStages, KC, TWO_D>(a, blockIdx.x, sm);
 }
 

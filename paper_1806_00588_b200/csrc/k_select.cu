@@ -421,7 +421,7 @@ static __device__ void softmax_row(const SoftmaxArgs& a, int row) {
 }
 
 #ifndef LSB_BODIES_ONLY  // (k_step_fused.cu includes this file for its device functions)
-__global__ void __launch_bounds__(kSelT) k_softmax_topb(SoftmaxArgs a) {
+__global__ void __launch_bounds__(kSelT) k_softmax_topb(const __grid_constant__ SoftmaxArgs a) {
   pdl_wait();
   softmax_row(a, blockIdx.x);
 }
@@ -679,7 +679,7 @@ static __device__ void expand_sentence(const ExpandArgs& a, int s, unsigned char
 
 #ifndef LSB_BODIES_ONLY
 template <int NT>
-__global__ void __launch_bounds__(NT) k_expand(ExpandArgs a) {
+__global__ void __launch_bounds__(NT) k_expand(const __grid_constant__ ExpandArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   pdl_wait();
   expand_sentence(a, blockIdx.x, smem);

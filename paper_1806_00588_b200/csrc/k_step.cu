@@ -148,7 +148,7 @@ static __device__ void compact_sentence(const CompactArgs& a, int s, uint32_t* b
 }
 
 #ifndef LSB_BODIES_ONLY  // (k_step_fused.cu includes this file for its device functions)
-__global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
+__global__ void __launch_bounds__(1024) k_compact(const __grid_constant__ CompactArgs a) {
   extern __shared__ uint32_t bm_dyn[];  // nwords
   pdl_wait();
   compact_sentence(a, blockIdx.x, bm_dyn);
@@ -463,7 +463,7 @@ static __device__ void probe_row(const ProbeArgs& a, unsigned char* smem, int ro
 
 #ifndef LSB_BODIES_ONLY
 template <int NT>
-__global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(ProbeArgs a) {
+__global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 1536 / NT) k_probe_count(const __grid_constant__ ProbeArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   probe_row(a, smem, blockIdx.x, blockIdx.y);
 }
