@@ -22,6 +22,7 @@
 //      calls with more lists than the rank kernel holds in shared memory.
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "glibc_log.cuh"
 #include "k_step.cuh"
@@ -458,15 +459,19 @@ __device__ __forceinline__ long long word_of(const ExpandArgs& a, const uint32_t
 // One flat (child, float4) index space; each thread keeps 8 loads in flight
 // before storing (a load->store chain per element would serialise on
 // latency: the store could alias the next load).
-static __device__ void reorder_hidden(const ExpandArgs& a, int s, int count, const uint32_t* beams) {
+static __device__ void reorder_hidden(const ExpandArgs& a, int s, int count, const uint32_t* beams,
+                                      int part = 0, int nparts = 1) {
   const int d = a.d;
   const size_t rbase = static_cast<size_t>(s) * a.Bsent;
   const size_t obase = static_cast<size_t>(s) * a.topB;
   constexpr int U = 8;
   if ((d & 3) == 0) {
     const int d4 = d >> 2;
-    const int total = count * d4;
-    for (int q0 = threadIdx.x; q0 < total; q0 += U * blockDim.x) {
+    // this CTA's slice [q_lo, total) of the (child, float4) space
+    const int all = count * d4;
+    const int q_lo = static_cast<int>(static_cast<long long>(all) * part / nparts);
+    const int total = static_cast<int>(static_cast<long long>(all) * (part + 1) / nparts);
+    for (int q0 = q_lo + threadIdx.x; q0 < total; q0 += U * blockDim.x) {
       float4 t[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -486,8 +491,10 @@ static __device__ void reorder_hidden(const ExpandArgs& a, int s, int count, con
       }
     }
   } else {
-    const int total = count * d;
-    for (int q0 = threadIdx.x; q0 < total; q0 += U * blockDim.x) {
+    const int all = count * d;
+    const int q_lo = static_cast<int>(static_cast<long long>(all) * part / nparts);
+    const int total = static_cast<int>(static_cast<long long>(all) * (part + 1) / nparts);
+    for (int q0 = q_lo + threadIdx.x; q0 < total; q0 += U * blockDim.x) {
       float t[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -515,8 +522,11 @@ static __device__ void reorder_hidden(const ExpandArgs& a, int s, int count, con
 constexpr int kRankMaxLists = 128;
 
 // One sentence's expansion by the whole CTA (any blockDim); smem holds the
-// candidates (expand_smem_bytes). k_expand runs a CTA per sentence.
-static __device__ void expand_sentence(const ExpandArgs& a, int s, unsigned char* smem) {
+// candidates (expand_smem_bytes). k_expand runs nparts CTAs per sentence: each
+// ranks the candidates (the same bits), part 0 writes the choices, and each
+// copies its 1/nparts of the hidden-state reorder.
+static __device__ void expand_sentence(const ExpandArgs& a, int s, unsigned char* smem,
+                                       int part = 0, int nparts = 1) {
   __shared__ int s_off[kRankMaxLists + 1];
   __shared__ uint32_t s_beams[64];
   __shared__ int s_count;
@@ -662,19 +672,20 @@ static __device__ void expand_sentence(const ExpandArgs& a, int s, unsigned char
     const int rank = cr[e];
     const Cand me{cs[e], cb[e], cw[e]};
     if (rank < B) {
-      a.choices[static_cast<size_t>(s) * B + rank] =
-          lsb_choice{me.score, me.beam, 0u, static_cast<int64_t>(me.word)};
+      if (part == 0)
+        a.choices[static_cast<size_t>(s) * B + rank] =
+            lsb_choice{me.score, me.beam, 0u, static_cast<int64_t>(me.word)};
       if (rank < 64) s_beams[rank] = me.beam;
     }
   }
   const int count = min(B, total);
   if (threadIdx.x == 0) {
-    a.n_choices[s] = count;
+    if (part == 0) a.n_choices[s] = count;
     s_count = count;
   }
   __syncthreads();
   pdl_trigger();
-  if (a.hidden_out && a.hidden) reorder_hidden(a, s, min(s_count, 64), s_beams);
+  if (a.hidden_out && a.hidden) reorder_hidden(a, s, min(s_count, 64), s_beams, part, nparts);
 }
 
 #ifndef LSB_BODIES_ONLY
@@ -682,7 +693,7 @@ template <int NT>
 __global__ void __launch_bounds__(NT) k_expand(const __grid_constant__ ExpandArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   pdl_wait();
-  expand_sentence(a, blockIdx.x, smem);
+  expand_sentence(a, blockIdx.x, smem, blockIdx.y, gridDim.y);
 }
 
 size_t expand_smem_bytes(const ExpandArgs& a) {
@@ -1108,7 +1119,16 @@ lsb_status launch_expand(lsb_ctx* ctx, const ExpandArgs& a) {
     const bool wide = a.topB <= 16;
     auto* kern = wide ? k_expand<1024> : k_expand<512>;
     if (lsb_status rc = ensure_smem(ctx, kern, rank_smem)) return rc;
-    LSB_CUDA(launch_pdl(ctx, kern, dim3(a.S), dim3(wide ? 1024 : 512), rank_smem, a));
+    // few sentences: several CTAs per sentence share the hidden reorder
+    // (each re-ranks the same candidates). Measured (B200, cfg 2 S=64: 1 / 2 /
+    // 4 / 8 parts 13.6 / 12.4 / 18.5 / 28.6 us; cfg 1 S=1: 37.7 -> 36.9 us per
+    // step at 8): the ranking, not the copy, bounds K5b, so only mildly.
+    static const int parts_env = getenv("LSB_K5B_PARTS") ? atoi(getenv("LSB_K5B_PARTS")) : 0;
+    const int parts = parts_env > 0                  ? parts_env
+                      : 16 * a.S <= ctx->sm_count    ? 8
+                      : 2 * a.S <= ctx->sm_count     ? 2
+                                                     : 1;
+    LSB_CUDA(launch_pdl(ctx, kern, dim3(a.S, parts), dim3(wide ? 1024 : 512), rank_smem, a));
     LSB_LAUNCHED(ctx, "k_expand");
     return LSB_OK;
   }
