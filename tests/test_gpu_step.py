@@ -376,12 +376,15 @@ def test_fast_step_tensor_cores(ctx, oracle, full):
     assert agree >= 0.99 * total, (agree, total)
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("mode", [0, 1])
-def test_graph_replay_equals_step(oracle, mode):
+def test_graph_replay_equals_step(oracle, monkeypatch, mode, fused):
     """lsb_batch_graph_capture / _launch: a replayed step on the captured
     buffers gives the eager step's choices, candidates and hidden reorder,
-    also after the buffers are rewritten in place (the decode-loop pattern)."""
+    also after the buffers are rewritten in place (the decode-loop pattern).
+    fused: the captured step is the single cooperative launch (LSB_FUSED=1)."""
     import torch
+    monkeypatch.setenv("LSB_FUSED", "1" if fused else "0")
 
     from paper_1806_00588_b200 import Batch, Context, Index, Model
     s = torch.cuda.Stream()
@@ -411,7 +414,10 @@ def test_graph_replay_equals_step(oracle, mode):
         s.synchronize()
 
     load(states[0])
+    n0 = ctx.launches
     b.graph_capture(H, sc, fin, nh, ch, nc, ho)
+    if fused:
+        assert ctx.launches - n0 == 1  # the captured step is one cooperative launch
     for st in states:
         load(st)
         with torch.cuda.stream(s):
