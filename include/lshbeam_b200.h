@@ -356,6 +356,10 @@ lsb_status lsb_measure_fp32x2_peak(lsb_ctx* ctx, double* lane_ops_per_s);
  * cum + log(p) in src/beam_decoder.cpp is evaluated by the host libm).
  * Device pointers; synchronises the context stream. */
 lsb_status lsb_selftest_log(lsb_ctx* ctx, const float* p_dev, double* out_dev, size_t n);
+/* Self-test: out_dev[k] = exp(x_dev[k]) by the device function the softmax
+ * uses (glibc's exp, bit for bit; src/beam_decoder.cpp:46-74 evaluates
+ * exp((double) l - mx) with the host libm). */
+lsb_status lsb_selftest_exp(lsb_ctx* ctx, const double* x_dev, double* out_dev, size_t n);
 
 /* ---------------------------------- 8. vocabulary-sharded step (cfg 4)
  * One rank's share of a decode step when E is split by contiguous vocabulary

@@ -128,6 +128,7 @@ _SIGS = [
     ("lsb_step_hidden", C.c_int, [VP, VP, VP, VP, U32, VP]),
     ("lsb_measure_fp32x2_peak", C.c_int, [VP, C.POINTER(C.c_double)]),
     ("lsb_selftest_log", C.c_int, [VP, VP, VP, C.c_size_t]),
+    ("lsb_selftest_exp", C.c_int, [VP, VP, VP, C.c_size_t]),
     ("lsb_exact_topb", C.c_int, [VP, VP, VP, C.c_int, C.c_int, C.c_int, C.c_int, VP, VP]),
     # vocabulary-sharded step
     ("lsb_shard_width", C.c_int, [VP]),

@@ -22,6 +22,7 @@ struct lsb_batch {
   int levels = -1;  // bit-sliced hit counting when 1 <= t <= 8
   int nspec = 0;
   int keep_probs = 0;
+  int seq_denom = 0;  // test hook: LSB_SEQ_DENOM=1 at create (SoftmaxArgs::seq_denominator)
   // device scratch
   uint32_t* specials = nullptr;
   uint32_t* qcodes = nullptr;

@@ -19,6 +19,12 @@ __global__ void k_selftest_log(const float* __restrict__ p, double* __restrict__
     out[k] = lsb::glibc_log(static_cast<double>(p[k]));
 }
 
+__global__ void k_selftest_exp(const double* __restrict__ x, double* __restrict__ out, size_t n) {
+  for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<size_t>(gridDim.x) * blockDim.x)
+    out[k] = lsb::glibc_exp(x[k]);
+}
+
 constexpr int kCalChains = 16, kCalIters = 2048;
 
 __global__ void __launch_bounds__(128) k_fp32x2_peak(unsigned long long* out,
@@ -94,6 +100,19 @@ extern "C" lsb_status lsb_selftest_log(lsb_ctx* ctx, const float* p_dev, double*
   LSB_CUDA(cudaSetDevice(ctx->device));
   k_selftest_log<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(p_dev, out_dev, n);
   LSB_LAUNCHED(ctx, "k_selftest_log");
+  LSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LSB_OK;
+}
+
+// Self-test of the device exp the softmax uses (glibc_log.cuh: glibc_exp):
+// out[k] = exp(x[k]) for n doubles in device memory (synchronised).
+extern "C" lsb_status lsb_selftest_exp(lsb_ctx* ctx, const double* x_dev, double* out_dev,
+                                       size_t n) {
+  if (!ctx || (n && (!x_dev || !out_dev))) return lsb::set_error("lsb_selftest_exp: null"), LSB_EINVAL;
+  if (n == 0) return LSB_OK;
+  LSB_CUDA(cudaSetDevice(ctx->device));
+  k_selftest_exp<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(x_dev, out_dev, n);
+  LSB_LAUNCHED(ctx, "k_selftest_exp");
   LSB_CUDA(cudaStreamSynchronize(ctx->stream));
   return LSB_OK;
 }

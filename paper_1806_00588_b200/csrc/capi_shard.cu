@@ -22,6 +22,7 @@
 #include <cfloat>
 
 #include "batch.cuh"
+#include "glibc_log.cuh"
 
 namespace lsb {
 
@@ -62,6 +63,9 @@ __global__ void __launch_bounds__(kShT) k_shard_exp(float* __restrict__ logits, 
                                                     const float* __restrict__ allmax, int G,
                                                     double* __restrict__ rowsum) {
   __shared__ double red[kShT / 32];
+  __shared__ unsigned long long exptab[256];
+  stage_exp_table(exptab);
+  __syncthreads();
   const int row = blockIdx.x, s = row / Bsent, i = row % Bsent;
   const bool live = !(n_hyp && i >= n_hyp[s]) && !(finished && finished[row]);
   const uint32_t n = live ? n_cand[s] : 0;
@@ -75,7 +79,7 @@ __global__ void __launch_bounds__(kShT) k_shard_exp(float* __restrict__ logits, 
   if (!(isinf(m) && m < 0)) {
     const double dm = static_cast<double>(m);
     for (uint32_t r = threadIdx.x; r < n; r += kShT) {
-      const double e = exp(static_cast<double>(L[r]) - dm);
+      const double e = glibc_exp_smem(static_cast<double>(L[r]) - dm, exptab);
       L[r] = static_cast<float>(e);
       sum += e;
     }

@@ -131,6 +131,7 @@ SoftmaxArgs lsb::softmax_args(const lsb_batch* b, const lsb_state_dev* in) {
   sa.top = b->top;
   sa.top_n = b->top_n;
   sa.err = b->ctx->err_dev;
+  sa.seq_denominator = b->seq_denom;
   return sa;
 }
 
@@ -228,6 +229,10 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
   b->mode = cfg->mode;
   // kTopOnly ignores t and scores [0,T) U specials (src/beam_decoder.cpp:189-199)
   b->cmode = cfg->full_vocab ? 2 : (!cfg->top_only && cfg->threshold == 0 ? 1 : 0);
+  {
+    const char* sd = getenv("LSB_SEQ_DENOM");
+    b->seq_denom = sd && atoi(sd) == 1;
+  }
   b->n_shared = b->cmode ? V : b->T;
   b->ncap = (static_cast<size_t>(V) + 3) & ~size_t(3);
   b->nwords = (V + 31) / 32;

@@ -6,7 +6,8 @@
 //
 // The includer defines LSB_LOG_FN (the function head), LSB_FMA(a, b, c) =
 // a * b + c rounded once, LSB_MUL / LSB_ADD / LSB_SUB rounded, LSB_AS_U64 /
-// LSB_AS_F64 bit casts and LSB_LOAD(table, i). One source for the device
+// LSB_AS_F64 bit casts, LSB_CONST(array, i) for constant indices and
+// LSB_LOAD(table, i) for data-dependent ones. One source for the device
 // function (glibc_log.cuh) and the CPU check against libm itself
 // (tests/glibc_log_check.c: every positive float <= 1, bit for bit).
 LSB_LOG_FN {
@@ -16,12 +17,12 @@ LSB_LOG_FN {
     if (ix == LSB_AS_U64(1.0)) return 0.0;
     const double r = LSB_SUB(x, 1.0);
     const double r2 = LSB_MUL(r, r), r3 = LSB_MUL(r, r2);
-    const double t1 = LSB_FMA(r2, LSB_LOAD(kLogPoly1, 3), LSB_FMA(r, LSB_LOAD(kLogPoly1, 2), LSB_LOAD(kLogPoly1, 1)));
-    const double t2 = LSB_FMA(r2, LSB_LOAD(kLogPoly1, 6), LSB_FMA(r, LSB_LOAD(kLogPoly1, 5), LSB_LOAD(kLogPoly1, 4)));
-    const double t3 = LSB_FMA(r3, LSB_LOAD(kLogPoly1, 10),
-                              LSB_FMA(r2, LSB_LOAD(kLogPoly1, 9), LSB_FMA(r, LSB_LOAD(kLogPoly1, 8), LSB_LOAD(kLogPoly1, 7))));
+    const double t1 = LSB_FMA(r2, LSB_CONST(kLogPoly1, 3), LSB_FMA(r, LSB_CONST(kLogPoly1, 2), LSB_CONST(kLogPoly1, 1)));
+    const double t2 = LSB_FMA(r2, LSB_CONST(kLogPoly1, 6), LSB_FMA(r, LSB_CONST(kLogPoly1, 5), LSB_CONST(kLogPoly1, 4)));
+    const double t3 = LSB_FMA(r3, LSB_CONST(kLogPoly1, 10),
+                              LSB_FMA(r2, LSB_CONST(kLogPoly1, 9), LSB_FMA(r, LSB_CONST(kLogPoly1, 8), LSB_CONST(kLogPoly1, 7))));
     const double p = LSB_FMA(LSB_FMA(t3, r3, t2), r3, t1);
-    const double b0 = LSB_LOAD(kLogPoly1, 0);
+    const double b0 = LSB_CONST(kLogPoly1, 0);
     const double rhi = LSB_FMA(-r, 0x1p27, LSB_FMA(r, 0x1p27, r));
     const double rlo = LSB_SUB(r, rhi);
     const double rhi2 = LSB_MUL(rhi, rhi);
@@ -45,12 +46,12 @@ LSB_LOG_FN {
   const double invc = LSB_LOAD(kLogTab, 2 * i), logc = LSB_LOAD(kLogTab, 2 * i + 1);
   const double r = LSB_FMA(z, invc, -1.0);
   const double kd = static_cast_f64(k);
-  const double w = LSB_FMA(kd, LSB_LOAD(kLogLn2, 0), logc);
+  const double w = LSB_FMA(kd, LSB_CONST(kLogLn2, 0), logc);
   const double r2 = LSB_MUL(r, r);
   const double hi = LSB_ADD(w, r);
-  const double lo = LSB_FMA(kd, LSB_LOAD(kLogLn2, 1), LSB_ADD(LSB_SUB(w, hi), r));
+  const double lo = LSB_FMA(kd, LSB_CONST(kLogLn2, 1), LSB_ADD(LSB_SUB(w, hi), r));
   const double r3 = LSB_MUL(r, r2);
-  const double q = LSB_FMA(r2, LSB_FMA(r, LSB_LOAD(kLogPoly, 4), LSB_LOAD(kLogPoly, 3)),
-                           LSB_FMA(r, LSB_LOAD(kLogPoly, 2), LSB_LOAD(kLogPoly, 1)));
-  return LSB_ADD(LSB_FMA(q, r3, LSB_FMA(r2, LSB_LOAD(kLogPoly, 0), lo)), hi);
+  const double q = LSB_FMA(r2, LSB_FMA(r, LSB_CONST(kLogPoly, 4), LSB_CONST(kLogPoly, 3)),
+                           LSB_FMA(r, LSB_CONST(kLogPoly, 2), LSB_CONST(kLogPoly, 1)));
+  return LSB_ADD(LSB_FMA(q, r3, LSB_FMA(r2, LSB_CONST(kLogPoly, 0), lo)), hi);
 }

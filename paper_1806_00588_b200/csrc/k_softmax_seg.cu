@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cfloat>
 
+#include "glibc_log.cuh"
 #include "k_step.cuh"
 
 namespace lsb {
@@ -140,6 +141,8 @@ __global__ void __launch_bounds__(kSegT) k_seg_max(SegArgs g) {
 __global__ void __launch_bounds__(kSegT) k_seg_exp(SegArgs g) {
   __shared__ double red[kSegT / 32];
   __shared__ float redf[kSegT / 32];
+  __shared__ unsigned long long exptab[256];  // published by seg_row_max's barriers
+  stage_exp_table(exptab);
   pdl_wait();
   int row, p;
   uint32_t c0, c1, n;
@@ -161,7 +164,7 @@ __global__ void __launch_bounds__(kSegT) k_seg_exp(SegArgs g) {
     for (int k = 0; k < 4; ++k) v[k] = L[c + k * kSegT];
     double e[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) e[k] = exp(static_cast<double>(v[k]) - dmx);
+    for (int k = 0; k < 4; ++k) e[k] = glibc_exp_smem(static_cast<double>(v[k]) - dmx, exptab);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       L[c + k * kSegT] = static_cast<float>(e[k]);
@@ -169,7 +172,7 @@ __global__ void __launch_bounds__(kSegT) k_seg_exp(SegArgs g) {
     }
   }
   for (; c < c1; c += kSegT) {
-    const double e = exp(static_cast<double>(L[c]) - dmx);
+    const double e = glibc_exp_smem(static_cast<double>(L[c]) - dmx, exptab);
     L[c] = static_cast<float>(e);
     sum += e;
   }

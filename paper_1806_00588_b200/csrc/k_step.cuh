@@ -81,6 +81,8 @@ struct SoftmaxArgs {
   TopEntry* top;           // [R_total][topB]
   int32_t* top_n;          // [R_total]
   uint32_t* err;
+  int seq_denominator;     // test hook (LSB_SEQ_DENOM=1): always take the
+                           // sequential-denominator path (reference_inv_*)
 };
 
 // K5b: per-sentence top-B merge by (score desc, beam asc, word asc) +

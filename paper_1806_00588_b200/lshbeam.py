@@ -85,6 +85,11 @@ class Context:
         (lsb_selftest_log); device pointers."""
         N.check(self.lib.lsb_selftest_log(self.h, p_dev, out_dev, n), "lsb_selftest_log")
 
+    def selftest_exp(self, x_dev: int, out_dev: int, n: int):
+        """out[k] = exp(x[k]) by the device's glibc-exact exp (lsb_selftest_exp);
+        device pointers to doubles."""
+        N.check(self.lib.lsb_selftest_exp(self.h, x_dev, out_dev, n), "lsb_selftest_exp")
+
     @property
     def launches(self) -> int:
         return int(self.lib.lsb_ctx_launch_count(self.h))

@@ -164,6 +164,15 @@ def test_fused_small_step_matches_oracle(ctx, oracle, monkeypatch, mode, V, d, K
     b2.close()
 
 
+@pytest.mark.parametrize("V,d,K,u,W,S,B,T,t", [CASES[0], CASES[6], CASES[8]])
+def test_step_sequential_denominator(ctx, oracle, monkeypatch, V, d, K, u, W, S, B, T, t):
+    """The softmax's sequential-denominator path (taken when the tree sum
+    cannot certify float(1/denom), ~1e-5 of rows) forced on every row
+    (LSB_SEQ_DENOM=1): the step still equals the oracle bit for bit."""
+    monkeypatch.setenv("LSB_SEQ_DENOM", "1")
+    test_step_matches_oracle(ctx, oracle, V, d, K, u, W, S, B, T, t, True)
+
+
 def test_step_config1_shape(ctx, oracle):
     """BASELINE config 1 shapes: V=40k, d=1000, B=12, K=8, u=3, W=16, T=1000, t=2."""
     V, d, K, u, W, B, T, t, S = 40000, 1000, 8, 3, 16, 12, 1000, 2, 2
