@@ -577,6 +577,10 @@ static lsb_status launch_logits_survivors(lsb_ctx* ctx, LogitsArgs a, lsb_mode m
   // lanes, 3x8 half-outputs per lane with 8-byte loads (22 instead of 28
   // wavefronts per 48 FFMA2, bit-exact) 105 us; 3x2 lanes (64-column tiles) at
   // 5 CTAs/SM 125 us; 16-float chunks in a 4-deep ring at 5 CTAs/SM 113 us.
+  // (Also measured: the whole per-sentence candidate list -- the identity
+  // block [0, T) is its prefix -- as survivor tiles only, 128 columns, so no
+  // part-filled block/survivor tile boundary: cfg 2 K4 102.1 vs 102.5 us but
+  // 502 vs 504 k sentence-steps/s, and S=128 231 vs 186 us.)
   // Small batches (a few sentences) fill a fraction of the GPU and each CTA
   // waits on its chunk loads: 32-column tiles (4x the CTAs) and an 8-deep ring.
   // (Measured, cfg 2 shapes: S=1 36 -> 18 us, S=8 49 -> 29, S=16 66 -> 49,
