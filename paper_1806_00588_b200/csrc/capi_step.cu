@@ -242,6 +242,8 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
     if (b->t >= 1 && b->t <= 8) {
       // t bit planes of the slice (t-1 levels + the marked set), <= 32 KB
       b->levels = b->t - 1;
+      // (cfg 4, V=200k -> 2 slices per row: 32 KB of planes measured best,
+      // 16 / 64 / 96 KB: probe 47.6 / 36.4 / 37.4 vs 33.3 us)
       const uint32_t budget = 32 * 1024 * 8 / b->t;  // words per slice
       const uint32_t nslices = (V + budget - 1) / budget;
       b->slice_len = ((V + nslices - 1) / nslices + 127) & ~127u;  // planes of 16-B multiples
