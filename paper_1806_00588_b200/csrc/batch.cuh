@@ -22,7 +22,7 @@ struct lsb_batch {
   int levels = -1;  // bit-sliced hit counting when 1 <= t <= 8
   int nspec = 0;
   int keep_probs = 0;
-  int seq_denom = 0;  // test hook: LSB_SEQ_DENOM=1 at create (SoftmaxArgs::seq_denominator)
+  int seq_denom = 0;  // test hook: LSB_SEQ_DENOM=1|2 at create (SoftmaxArgs::seq_denominator)
   // device scratch
   uint32_t* specials = nullptr;
   uint32_t* qcodes = nullptr;
@@ -49,6 +49,8 @@ struct lsb_batch {
   lsb::TopEntry* seg_top = nullptr;
   int32_t* seg_n = nullptr;
   uint32_t* seg_count = nullptr;
+  float* seg_e = nullptr;            // [S*B][ncap] float(e): the logits stay intact
+  float* seg_inv = nullptr;          // [S*B] float(1/denom), the reference's
   lsb::TopEntry* sh_top = nullptr;   // vocabulary-sharded step: local top-B'
   int32_t* sh_topn = nullptr;
   // small batches: the whole step as one cooperative launch (k_step_fused.cu)

@@ -29,7 +29,8 @@ lsb_status free_batch(lsb_batch* b) {
                   b->prov,     b->logits,   b->top,        b->top_n,        b->h_hidden,
                   b->h_scores, b->h_finished, b->h_nhyp,   b->h_choices,    b->h_nchoices,
                   b->h_hidden_out, b->sh_top, b->sh_topn, b->tc_A, b->tc_H, b->arrive,
-                  b->seg_max, b->seg_sum, b->seg_top, b->seg_n, b->seg_count,
+                  b->seg_max, b->seg_sum, b->seg_top, b->seg_n, b->seg_count, b->seg_e,
+                  b->seg_inv,
                   b->split_cnt, b->split_arrive};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -231,7 +232,7 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
   b->cmode = cfg->full_vocab ? 2 : (!cfg->top_only && cfg->threshold == 0 ? 1 : 0);
   {
     const char* sd = getenv("LSB_SEQ_DENOM");
-    b->seq_denom = sd && atoi(sd) == 1;
+    b->seq_denom = sd ? atoi(sd) : 0;  // 1: always sequential, 2: tier 2 first
   }
   b->n_shared = b->cmode ? V : b->T;
   b->ncap = (static_cast<size_t>(V) + 3) & ~size_t(3);
@@ -314,6 +315,8 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
     if (e == cudaSuccess) e = dalloc(&b->seg_n, np);
     if (e == cudaSuccess) e = dalloc(&b->seg_count, SB);
     if (e == cudaSuccess) e = cudaMemset(b->seg_count, 0, SB * sizeof(uint32_t));
+    if (e == cudaSuccess) e = dalloc(&b->seg_e, SB * b->ncap);
+    if (e == cudaSuccess) e = dalloc(&b->seg_inv, SB);
   }
   // FAST: the rows sharing [0, n_shared) form a dense contraction for the
   // tensor cores; E's block is split into 3xTF32 and tiled once, here
@@ -438,6 +441,8 @@ lsb_status lsb_step(lsb_batch* b, const lsb_state_dev* in, const lsb_out_dev* ou
     g.seg_top = b->seg_top;
     g.seg_n = b->seg_n;
     g.count = b->seg_count;
+    g.e_out = b->seg_e;
+    g.inv = b->seg_inv;
     if ((rc = launch_softmax_seg(ctx, g))) return rc;
     if (b->rec) LSB_CUDA(cudaEventRecord(b->ev[4], st));
     if ((rc = launch_expand(ctx, ea))) return rc;

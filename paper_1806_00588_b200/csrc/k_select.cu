@@ -26,6 +26,7 @@
 
 #include "glibc_log.cuh"
 #include "k_step.cuh"
+#include "softmax_denom.cuh"
 
 namespace lsb {
 
@@ -120,74 +121,7 @@ __device__ __forceinline__ float kth_lane_max(float x, int K) {
 }
 
 
-// ------------------------------------------ the reference's softmax denominator
-// src/beam_decoder.cpp:46-74 sums e_j = exp(l_j - mx) in double SEQUENTIALLY
-// in column order, then inv = float(1 / denom). The device sums the same e_j
-// in a tree (per-thread runs, then a warp / block reduction). For sums of
-// non-negative terms the sequential sum is within (n - 1) u S and the tree
-// within depth * u S of the exact S (u = 2^-53), so the two are within
-// tol = (n + 64) 2^-52 * tree of each other. float(1 / x) is monotone in x:
-// when both ends of [tree - tol, tree + tol] round to the same float, that
-// float IS the reference's inv. Otherwise -- about (n 2^-52) / 2^-24, i.e.
-// 1e-5 of rows of 1-2k candidates -- the sum is redone sequentially: e_j
-// recomputed from the (still unmodified) logits, a CTA / warp at a time, one
-// running sum added in column order.
-__device__ __forceinline__ bool inv_certified(double tree, uint32_t n, int force_seq, float* inv) {
-  const double tol = static_cast<double>(n + 64) * 0x1p-52 * tree;
-  const float lo = static_cast<float>(1.0 / (tree + tol));
-  const float hi = static_cast<float>(1.0 / (tree - tol));
-  *inv = lo;
-  return lo == hi && !force_seq;
-}
-
-// The sequential sum by the CTA (kSelT threads): e_j recomputed 128 at a time
-// into shared memory, thread 0 adding them in column order. Out of line: rare.
-static __device__ __noinline__ float sequential_inv_cta(uint32_t n, const float* L, double dmx) {
-  __shared__ double s_e[kSelT];
-  __shared__ float s_inv;
-  double seq = 0.0;
-  for (uint32_t c0 = 0; c0 < n; c0 += kSelT) {
-    const uint32_t c = c0 + threadIdx.x;
-    __syncthreads();  // the previous round's s_e has been added
-    s_e[threadIdx.x] = c < n ? glibc_exp(static_cast<double>(L[c]) - dmx) : 0.0;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const uint32_t m = min(static_cast<uint32_t>(kSelT), n - c0);
-      for (uint32_t k = 0; k < m; ++k) seq = __dadd_rn(seq, s_e[k]);
-    }
-  }
-  if (threadIdx.x == 0) s_inv = static_cast<float>(1.0 / seq);
-  __syncthreads();
-  return s_inv;
-}
-
-// CTA-wide (uniform arguments); L = the row's logits, still unmodified.
-__device__ __forceinline__ float reference_inv_cta(double tree, uint32_t n, const float* L,
-                                                   double dmx, int force_seq) {
-  float inv;
-  if (inv_certified(tree, n, force_seq, &inv)) return inv;
-  return sequential_inv_cta(n, L, dmx);
-}
-
-// Warp-wide (the fused K5's warp per row): every lane adds the same shuffled
-// terms, so every lane ends with the reference's sum.
-static __device__ __noinline__ float sequential_inv_warp(uint32_t n, const float* L, double dmx,
-                                                         int lane) {
-  double seq = 0.0;
-  for (uint32_t c0 = 0; c0 < n; c0 += 32) {
-    const uint32_t c = c0 + lane;
-    const double e = c < n ? glibc_exp(static_cast<double>(L[c]) - dmx) : 0.0;
-    const int m = static_cast<int>(min(32u, n - c0));
-    for (int k = 0; k < m; ++k) seq = __dadd_rn(seq, __shfl_sync(0xffffffffu, e, k));
-  }
-  return static_cast<float>(1.0 / seq);
-}
-__device__ __forceinline__ float reference_inv_warp(double tree, uint32_t n, const float* L,
-                                                    double dmx, int lane, int force_seq) {
-  float inv;
-  if (inv_certified(tree, n, force_seq, &inv)) return inv;
-  return sequential_inv_warp(n, L, dmx, lane);
-}
+// The reference's softmax denominator: softmax_denom.cuh.
 
 // Rows of at most kSelT * kSelReg candidates (the LSH step's): the row lives
 // in registers, kSelReg values per thread -- one global read, no exp/prob
@@ -232,7 +166,7 @@ __device__ __forceinline__ void row_registers(const SoftmaxArgs& a, int row, flo
     }
   }
   sum = block_reduce<double, decltype(dsum_op), true>(sum, red_d, dsum_op);
-  const float inv = reference_inv_cta(sum, n, L, dmx, a.seq_denominator);
+  const float inv = reference_inv_cta<kSelT>(sum, n, L, dmx, a.seq_denominator);
 #pragma unroll
   for (int k = 0; k < REG; ++k) {
     const uint32_t c = tid + kSelT * k;
@@ -383,7 +317,7 @@ static __device__ void softmax_row(const SoftmaxArgs& a, int row) {
     for (uint32_t r = tid; r < n; r += kSelT)
       sum += glibc_exp_smem(static_cast<double>(L[r]) - dmx, s_exptab);
     sum = block_reduce<double, decltype(dsum_op), true>(sum, red_d, dsum_op);
-    inv = reference_inv_cta(sum, n, L, dmx, a.seq_denominator);
+    inv = reference_inv_cta<kSelT>(sum, n, L, dmx, a.seq_denominator);
     // (the logits are needed until inv is known: float(e) replaces them now)
     for (uint32_t r = tid; r < n; r += kSelT)
       L[r] = static_cast<float>(glibc_exp_smem(static_cast<double>(L[r]) - dmx, s_exptab));

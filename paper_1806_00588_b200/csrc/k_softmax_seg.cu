@@ -3,24 +3,28 @@
 // so the 12 rows of a one-sentence full-vocabulary step spread over the whole
 // GPU instead of 12 CTAs (S=1, V=40k: 150 us in k_softmax_topb).
 //
-// softmax_rows (src/beam_decoder.cpp:46-74) in three launches:
+// softmax_rows (src/beam_decoder.cpp:46-74) in four launches:
 //   k_seg_max    : segment float max -> part_max[row][p]
 //   k_seg_exp    : row max = max over the P partials (float max is exact in
-//                  any order); e = exp((double)l - mx), stored as float(e);
+//                  any order); e = exp((double)l - mx) (glibc's exp), stored
+//                  as float(e) in a separate buffer (the logits stay intact);
 //                  segment double sum -> part_sum[row][p]
-//   k_seg_select : denominator = sum of the P partials in segment order;
-//                  p = float(e) * float(1/denom) (written back when kept);
-//                  segment top-B by (p desc, column asc) with the threshold
-//                  selection of k_softmax_topb; the row's last segment CTA to
-//                  finish merges the P sorted lists into the row's top-B.
-// The double denominator is a fixed-shape tree (deterministic), like
-// k_softmax_topb's; its order differs from the reference's sequential sum,
-// which the probability tests tolerate at the size / 1e5 bit level.
+//   k_seg_denom  : one CTA per row: the P partials in segment order, then the
+//                  certified float(1/denom) -- equal to the reference's
+//                  sequential sum's, else redone sequentially from the logits
+//                  (softmax_denom.cuh) -> inv[row]
+//   k_seg_select : p = float(e) * inv (written back into the logits when
+//                  kept); segment top-B by (p desc, column asc) with the
+//                  threshold selection of k_softmax_topb; the row's last
+//                  segment CTA to finish merges the P sorted lists into the
+//                  row's top-B.
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "glibc_log.cuh"
 #include "k_step.cuh"
+#include "softmax_denom.cuh"
 
 namespace lsb {
 
@@ -152,7 +156,8 @@ __global__ void __launch_bounds__(kSegT) k_seg_exp(SegArgs g) {
     if (threadIdx.x == 0 && p == 0) atomicOr(g.sa.err, kErrEmptyRow);
     return;
   }
-  float* L = g.sa.logits + static_cast<size_t>(row) * g.sa.ldl;
+  const float* L = g.sa.logits + static_cast<size_t>(row) * g.sa.ldl;
+  float* Eo = g.e_out + static_cast<size_t>(row) * g.sa.ldl;
   const double dmx = static_cast<double>(mx);
   double sum = 0.0;
   // four independent loads / exps in flight per thread; the sum keeps the
@@ -167,18 +172,44 @@ __global__ void __launch_bounds__(kSegT) k_seg_exp(SegArgs g) {
     for (int k = 0; k < 4; ++k) e[k] = glibc_exp_smem(static_cast<double>(v[k]) - dmx, exptab);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      L[c + k * kSegT] = static_cast<float>(e[k]);
+      Eo[c + k * kSegT] = static_cast<float>(e[k]);
       sum += e[k];
     }
   }
   for (; c < c1; c += kSegT) {
     const double e = glibc_exp_smem(static_cast<double>(L[c]) - dmx, exptab);
-    L[c] = static_cast<float>(e);
+    Eo[c] = static_cast<float>(e);
     sum += e;
   }
   sum = seg_reduce(sum, red, SegDSum{});
   pdl_trigger();
   if (threadIdx.x == 0) g.part_sum[blockIdx.x] = sum;
+}
+
+// One CTA per row: the row's denominator from the P segment partials (in
+// segment order), certified against the reference's sequential sum or redone
+// sequentially from the intact logits; inv[row] for k_seg_select.
+__global__ void __launch_bounds__(kSegT) k_seg_denom(SegArgs g) {
+  __shared__ float redf[kSegT / 32];
+  __shared__ double s_part[kSegMaxP];
+  const SoftmaxArgs& a = g.sa;
+  pdl_wait();
+  const int row = blockIdx.x;
+  const int s = row / a.Bsent, i = row % a.Bsent;
+  if ((a.n_hyp && i >= a.n_hyp[s]) || (a.finished && a.finished[row])) return;
+  const uint32_t n = a.n_cand ? a.n_cand[s] : a.n_const;
+  const float mx = seg_row_max(g, row, redf);
+  if (n == 0 || (isinf(mx) && mx < 0)) return;
+  for (int q = threadIdx.x; q < g.P; q += kSegT) s_part[q] = g.part_sum[row * g.P + q];
+  __syncthreads();
+  double denom = 0.0;
+  for (int q = 0; q < g.P; ++q) denom += s_part[q];
+  // (the segment partials add P more levels to the tree: n + P bounds them)
+  const float inv = reference_inv_cta<kSegT, true>(denom, n, a.logits + static_cast<size_t>(row) * a.ldl,
+                                             static_cast<double>(mx), a.seq_denominator,
+                                             static_cast<uint32_t>(g.P));
+  pdl_trigger();
+  if (threadIdx.x == 0) g.inv[row] = inv;
 }
 
 __global__ void __launch_bounds__(kSegT) k_seg_select(SegArgs g) {
@@ -190,7 +221,6 @@ __global__ void __launch_bounds__(kSegT) k_seg_select(SegArgs g) {
   __shared__ uint32_t win_r[kSegT / 32];
   __shared__ bool s_last;
   __shared__ float redf[kSegT / 32];
-  __shared__ double s_part[kSegMaxP];
   __shared__ int s_off[kSegMaxP];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const SoftmaxArgs& a = g.sa;
@@ -208,22 +238,19 @@ __global__ void __launch_bounds__(kSegT) k_seg_select(SegArgs g) {
     if (tid == 0 && p == 0) a.top_n[row] = 0;
     return;
   }
-  // denominator: the P partials summed in segment order
-  for (int q = tid; q < g.P; q += kSegT) s_part[q] = g.part_sum[row * g.P + q];
-  __syncthreads();
-  double denom = 0.0;
-  for (int q = 0; q < g.P; ++q) denom += s_part[q];
-  const float inv = static_cast<float>(1.0 / denom);
+  // float(1/denom): k_seg_denom's (certified or sequential)
+  const float inv = g.inv[row];
   float* L = a.logits + static_cast<size_t>(row) * a.ldl;
+  const float* Eo = g.e_out + static_cast<size_t>(row) * a.ldl;
   const uint32_t m = c1 - c0;
   // pass 1: p (kept when asked) and each thread's maximum
   float x = -1.0f;
   for (uint32_t c = c0 + tid; c < c1; c += kSegT) {
-    const float pv = __fmul_rn(L[c], inv);
+    const float pv = __fmul_rn(Eo[c], inv);
     if (a.keep_probs) L[c] = pv;
     x = fmaxf(x, pv);
   }
-  auto p_at = [&](uint32_t c) { return a.keep_probs ? L[c] : __fmul_rn(L[c], inv); };
+  auto p_at = [&](uint32_t c) { return a.keep_probs ? L[c] : __fmul_rn(Eo[c], inv); };
   if (tid == 0) s_nc = 0;
   const float tau = seg_kth(x, B, s_lm);
   const int keep = static_cast<int>(min(static_cast<uint32_t>(B), m));
@@ -398,6 +425,8 @@ lsb_status launch_softmax_seg(lsb_ctx* ctx, const SegArgs& g) {
   LSB_LAUNCHED(ctx, "k_seg_max");
   LSB_CUDA(launch_pdl(ctx, k_seg_exp, grid, dim3(kSegT), 0, g));
   LSB_LAUNCHED(ctx, "k_seg_exp");
+  LSB_CUDA(launch_pdl(ctx, k_seg_denom, dim3(g.sa.R_total), dim3(kSegT), 0, g));
+  LSB_LAUNCHED(ctx, "k_seg_denom");
   LSB_CUDA(launch_pdl(ctx, k_seg_select, grid, dim3(kSegT), 0, g));
   LSB_LAUNCHED(ctx, "k_seg_select");
   return LSB_OK;

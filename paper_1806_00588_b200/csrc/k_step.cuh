@@ -81,8 +81,8 @@ struct SoftmaxArgs {
   TopEntry* top;           // [R_total][topB]
   int32_t* top_n;          // [R_total]
   uint32_t* err;
-  int seq_denominator;     // test hook (LSB_SEQ_DENOM=1): always take the
-                           // sequential-denominator path (reference_inv_*)
+  int seq_denominator;     // test hook (LSB_SEQ_DENOM): 1 = always the sequential
+                           // denominator, 2 = the tight interval first (softmax_denom.cuh)
 };
 
 // K5b: per-sentence top-B merge by (score desc, beam asc, word asc) +
@@ -148,6 +148,8 @@ struct SegArgs {
   TopEntry* seg_top;  // [R][P][topB]
   int32_t* seg_n;     // [R][P]
   uint32_t* count;    // [R], zero between steps (self-resetting)
+  float* e_out;       // [R][ldl] float(e) (the logits stay intact for the denominator)
+  float* inv;         // [R] float(1/denom), certified / sequential (k_seg_denom)
 };
 int seg_count(lsb_ctx* ctx, int R, uint32_t n, int B);
 lsb_status launch_softmax_seg(lsb_ctx* ctx, const SegArgs& g);

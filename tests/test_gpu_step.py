@@ -164,12 +164,14 @@ def test_fused_small_step_matches_oracle(ctx, oracle, monkeypatch, mode, V, d, K
     b2.close()
 
 
+@pytest.mark.parametrize("seq", ["1", "2"])
 @pytest.mark.parametrize("V,d,K,u,W,S,B,T,t", [CASES[0], CASES[6], CASES[8]])
-def test_step_sequential_denominator(ctx, oracle, monkeypatch, V, d, K, u, W, S, B, T, t):
-    """The softmax's sequential-denominator path (taken when the tree sum
-    cannot certify float(1/denom), ~1e-5 of rows) forced on every row
-    (LSB_SEQ_DENOM=1): the step still equals the oracle bit for bit."""
-    monkeypatch.setenv("LSB_SEQ_DENOM", "1")
+def test_step_sequential_denominator(ctx, oracle, monkeypatch, V, d, K, u, W, S, B, T, t, seq):
+    """The softmax denominator's rare paths (softmax_denom.cuh: the tight
+    interval when the tree sum's worst-case bound cannot certify
+    float(1/denom), the sequential sum when neither can) forced on every row
+    (LSB_SEQ_DENOM=2 / 1): the step still equals the oracle bit for bit."""
+    monkeypatch.setenv("LSB_SEQ_DENOM", seq)
     test_step_matches_oracle(ctx, oracle, V, d, K, u, W, S, B, T, t, True)
 
 
@@ -199,7 +201,12 @@ def test_step_config1_shape(ctx, oracle):
     (6000, 64, 4, 12), (5000, 128, 3, 10), (4100, 40, 5, 6),
     # V >= 8192: segmented K5a (P segments per row, last CTA merges)
     (9000, 64, 1, 12), (20000, 32, 3, 8)])
-def test_full_vocab_step(ctx, oracle, mode, V, d, S, B):
+@pytest.mark.parametrize("seq", ["0", "1", "2"])
+def test_full_vocab_step(ctx, oracle, monkeypatch, mode, V, d, S, B, seq):
+    """kFull vs the oracle: choices, and in PARITY every probability bit for
+    bit (the segmented K5a's certified denominator; seq=1 / 2 force its
+    sequential sum / its tight interval on every row)."""
+    monkeypatch.setenv("LSB_SEQ_DENOM", seq)
     E = oracle.gaussian(11, V * d).reshape(V, d)
     bias = oracle.synth_model(V, d, 11, 8.0, want=("bias",))["bias"]
     state = make_state(oracle, S, B, d, seed=5, frozen_every=4)
@@ -208,6 +215,9 @@ def test_full_vocab_step(ctx, oracle, mode, V, d, S, B):
     hidden, scores, finished, n_hyp = state
     for s in range(S):
         want = oracle_full_step(oracle, E, bias, hidden[s], scores[s], finished[s], B, B)
+        if mode == 0:
+            np.testing.assert_array_equal(b.probs(s).view(np.uint32),
+                                          want["probs"].view(np.uint32))
         ws, wb, ww = want["choices"]
         assert [c[2] for c in res[s]] == ww.tolist()
         assert [c[1] for c in res[s]] == wb.tolist()
