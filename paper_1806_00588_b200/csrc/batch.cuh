@@ -22,7 +22,7 @@ struct lsb_batch {
   int levels = -1;  // bit-sliced hit counting when 1 <= t <= 8
   int nspec = 0;
   int keep_probs = 0;
-  int seq_denom = 0;  // test hook: LSB_SEQ_DENOM=1|2 at create (SoftmaxArgs::seq_denominator)
+  int seq_denom = 0;  // test hook: LSB_SEQ_DENOM=1 at create (SoftmaxArgs::seq_denominator)
   // device scratch
   uint32_t* specials = nullptr;
   uint32_t* qcodes = nullptr;
@@ -46,6 +46,8 @@ struct lsb_batch {
   int seg_P = 0;
   float* seg_max = nullptr;
   double* seg_sum = nullptr;
+  double* seg_c = nullptr;
+  double* seg_b = nullptr;
   lsb::TopEntry* seg_top = nullptr;
   int32_t* seg_n = nullptr;
   uint32_t* seg_count = nullptr;

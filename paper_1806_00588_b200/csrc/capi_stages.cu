@@ -200,7 +200,7 @@ lsb_status lsb_softmax_rows(lsb_ctx* ctx, const float* logits_host, int rows, in
   sa.top = top.p;
   sa.top_n = topn.p;
   sa.err = ctx->err_dev;
-  sa.seq_denominator = getenv("LSB_SEQ_DENOM") ? atoi(getenv("LSB_SEQ_DENOM")) : 0;
+  sa.seq_denominator = getenv("LSB_SEQ_DENOM") && atoi(getenv("LSB_SEQ_DENOM")) == 1;
   lsb_status rc = launch_softmax(ctx, sa);
   if (rc) return rc;
   LSB_CUDA(cudaMemcpyAsync(out_host, L.p, static_cast<size_t>(rows) * n * 4, cudaMemcpyDeviceToHost, st));

@@ -29,7 +29,8 @@ lsb_status free_batch(lsb_batch* b) {
                   b->prov,     b->logits,   b->top,        b->top_n,        b->h_hidden,
                   b->h_scores, b->h_finished, b->h_nhyp,   b->h_choices,    b->h_nchoices,
                   b->h_hidden_out, b->sh_top, b->sh_topn, b->tc_A, b->tc_H, b->arrive,
-                  b->seg_max, b->seg_sum, b->seg_top, b->seg_n, b->seg_count, b->seg_e,
+                  b->seg_max, b->seg_sum, b->seg_c, b->seg_b, b->seg_top, b->seg_n,
+                  b->seg_count, b->seg_e,
                   b->seg_inv,
                   b->split_cnt, b->split_arrive};
   for (void* p : ptrs)
@@ -232,7 +233,7 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
   b->cmode = cfg->full_vocab ? 2 : (!cfg->top_only && cfg->threshold == 0 ? 1 : 0);
   {
     const char* sd = getenv("LSB_SEQ_DENOM");
-    b->seq_denom = sd ? atoi(sd) : 0;  // 1: always sequential, 2: tier 2 first
+    b->seq_denom = sd && atoi(sd) == 1;  // always the sequential sum
   }
   b->n_shared = b->cmode ? V : b->T;
   b->ncap = (static_cast<size_t>(V) + 3) & ~size_t(3);
@@ -311,6 +312,8 @@ lsb_status lsb_batch_create(lsb_ctx* ctx, const lsb_model* model, const lsb_inde
     const size_t np = SB * b->seg_P;
     e = dalloc(&b->seg_max, np);
     if (e == cudaSuccess) e = dalloc(&b->seg_sum, np);
+    if (e == cudaSuccess) e = dalloc(&b->seg_c, np);
+    if (e == cudaSuccess) e = dalloc(&b->seg_b, np);
     if (e == cudaSuccess) e = dalloc(&b->seg_top, np * b->B);
     if (e == cudaSuccess) e = dalloc(&b->seg_n, np);
     if (e == cudaSuccess) e = dalloc(&b->seg_count, SB);
@@ -438,6 +441,8 @@ lsb_status lsb_step(lsb_batch* b, const lsb_state_dev* in, const lsb_out_dev* ou
     g.seglen = static_cast<uint32_t>((b->V + b->seg_P - 1) / b->seg_P);
     g.part_max = b->seg_max;
     g.part_sum = b->seg_sum;
+    g.part_c = b->seg_c;
+    g.part_b = b->seg_b;
     g.seg_top = b->seg_top;
     g.seg_n = b->seg_n;
     g.count = b->seg_count;

@@ -8,11 +8,12 @@
 //   k_seg_exp    : row max = max over the P partials (float max is exact in
 //                  any order); e = exp((double)l - mx) (glibc's exp), stored
 //                  as float(e) in a separate buffer (the logits stay intact);
-//                  segment double sum -> part_sum[row][p]
-//   k_seg_denom  : one CTA per row: the P partials in segment order, then the
-//                  certified float(1/denom) -- equal to the reference's
-//                  sequential sum's, else redone sequentially from the logits
-//                  (softmax_denom.cuh) -> inv[row]
+//                  segment compensated sum (hi, c) and the bound
+//                  sum min(e, 2^-52) -> part_sum / part_c / part_b[row][p]
+//   k_seg_denom  : one CTA per row: the exact row sum and the bound give an
+//                  interval holding the reference's sequential sum; its
+//                  float(1/x) if both ends agree, else the sequential sum
+//                  redone from the logits (softmax_denom.cuh) -> inv[row]
 //   k_seg_select : p = float(e) * inv (written back into the logits when
 //                  kept); segment top-B by (p desc, column asc) with the
 //                  threshold selection of k_softmax_topb; the row's last
@@ -54,9 +55,6 @@ __device__ __forceinline__ T seg_reduce(T v, T* red, Op op) {
 
 struct SegFMax {
   __device__ float operator()(float x, float y) const { return (x < y) ? y : x; }
-};
-struct SegDSum {
-  __device__ double operator()(double x, double y) const { return x + y; }
 };
 
 // The row's (segment's) coordinates; false for rows that are not scored.
@@ -143,7 +141,6 @@ __global__ void __launch_bounds__(kSegT) k_seg_max(SegArgs g) {
 }
 
 __global__ void __launch_bounds__(kSegT) k_seg_exp(SegArgs g) {
-  __shared__ double red[kSegT / 32];
   __shared__ float redf[kSegT / 32];
   __shared__ unsigned long long exptab[256];  // published by seg_row_max's barriers
   stage_exp_table(exptab);
@@ -159,9 +156,9 @@ __global__ void __launch_bounds__(kSegT) k_seg_exp(SegArgs g) {
   const float* L = g.sa.logits + static_cast<size_t>(row) * g.sa.ldl;
   float* Eo = g.e_out + static_cast<size_t>(row) * g.sa.ldl;
   const double dmx = static_cast<double>(mx);
-  double sum = 0.0;
-  // four independent loads / exps in flight per thread; the sum keeps the
-  // thread's element order
+  // compensated sum (hi + c exact) and the sequential-error bound b
+  double hi = 0.0, cc = 0.0, bnd = 0.0;
+  // four independent loads / exps in flight per thread
   uint32_t c = c0 + threadIdx.x;
   for (; c + 3 * kSegT < c1; c += 4 * kSegT) {
     float v[4];
@@ -173,25 +170,49 @@ __global__ void __launch_bounds__(kSegT) k_seg_exp(SegArgs g) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       Eo[c + k * kSegT] = static_cast<float>(e[k]);
-      sum += e[k];
+      dd_add(hi, cc, e[k]);
+      bnd = __dadd_rn(bnd, fmin(e[k], 0x1p-52));
     }
   }
   for (; c < c1; c += kSegT) {
     const double e = glibc_exp_smem(static_cast<double>(L[c]) - dmx, exptab);
     Eo[c] = static_cast<float>(e);
-    sum += e;
+    dd_add(hi, cc, e);
+    bnd = __dadd_rn(bnd, fmin(e, 0x1p-52));
   }
-  sum = seg_reduce(sum, red, SegDSum{});
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    const double c2 = __shfl_xor_sync(0xffffffffu, cc, o);
+    dd_merge(hi, cc, h2, c2);
+    bnd = __dadd_rn(bnd, __shfl_xor_sync(0xffffffffu, bnd, o));
+  }
+  __shared__ double s_hi[kSegT / 32], s_c[kSegT / 32], s_b[kSegT / 32];
+  if ((threadIdx.x & 31) == 0) {
+    s_hi[threadIdx.x >> 5] = hi;
+    s_c[threadIdx.x >> 5] = cc;
+    s_b[threadIdx.x >> 5] = bnd;
+  }
+  __syncthreads();
   pdl_trigger();
-  if (threadIdx.x == 0) g.part_sum[blockIdx.x] = sum;
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kSegT / 32; ++w) {
+      dd_merge(hi, cc, s_hi[w], s_c[w]);
+      bnd = __dadd_rn(bnd, s_b[w]);
+    }
+    g.part_sum[blockIdx.x] = hi;
+    g.part_c[blockIdx.x] = cc;
+    g.part_b[blockIdx.x] = bnd;
+  }
 }
 
-// One CTA per row: the row's denominator from the P segment partials (in
-// segment order), certified against the reference's sequential sum or redone
-// sequentially from the intact logits; inv[row] for k_seg_select.
+// One CTA per row: the row's exact sum from the P compensated segment
+// partials and the sequential-error bound (softmax_denom.cuh), certified
+// float(1/denom) or the sequential sum from the intact logits; inv[row] for
+// k_seg_select.
 __global__ void __launch_bounds__(kSegT) k_seg_denom(SegArgs g) {
   __shared__ float redf[kSegT / 32];
-  __shared__ double s_part[kSegMaxP];
+  __shared__ double s_part[kSegMaxP], s_pc[kSegMaxP], s_pb[kSegMaxP];
   const SoftmaxArgs& a = g.sa;
   pdl_wait();
   const int row = blockIdx.x;
@@ -200,14 +221,21 @@ __global__ void __launch_bounds__(kSegT) k_seg_denom(SegArgs g) {
   const uint32_t n = a.n_cand ? a.n_cand[s] : a.n_const;
   const float mx = seg_row_max(g, row, redf);
   if (n == 0 || (isinf(mx) && mx < 0)) return;
-  for (int q = threadIdx.x; q < g.P; q += kSegT) s_part[q] = g.part_sum[row * g.P + q];
+  for (int q = threadIdx.x; q < g.P; q += kSegT) {
+    s_part[q] = g.part_sum[row * g.P + q];
+    s_pc[q] = g.part_c[row * g.P + q];
+    s_pb[q] = g.part_b[row * g.P + q];
+  }
   __syncthreads();
-  double denom = 0.0;
-  for (int q = 0; q < g.P; ++q) denom += s_part[q];
-  // (the segment partials add P more levels to the tree: n + P bounds them)
-  const float inv = reference_inv_cta<kSegT, true>(denom, n, a.logits + static_cast<size_t>(row) * a.ldl,
-                                             static_cast<double>(mx), a.seq_denominator,
-                                             static_cast<uint32_t>(g.P));
+  double hi = 0.0, cc = 0.0, bnd = 0.0;
+  for (int q = 0; q < g.P; ++q) {
+    dd_merge(hi, cc, s_part[q], s_pc[q]);
+    bnd = __dadd_rn(bnd, s_pb[q]);
+  }
+  float inv;
+  if (a.seq_denominator == 1 || !inv_from_exact(hi, cc, bnd, &inv))
+    inv = sequential_inv_cta<kSegT>(n, a.logits + static_cast<size_t>(row) * a.ldl,
+                                    static_cast<double>(mx));
   pdl_trigger();
   if (threadIdx.x == 0) g.inv[row] = inv;
 }

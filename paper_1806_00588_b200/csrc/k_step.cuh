@@ -81,8 +81,8 @@ struct SoftmaxArgs {
   TopEntry* top;           // [R_total][topB]
   int32_t* top_n;          // [R_total]
   uint32_t* err;
-  int seq_denominator;     // test hook (LSB_SEQ_DENOM): 1 = always the sequential
-                           // denominator, 2 = the tight interval first (softmax_denom.cuh)
+  int seq_denominator;     // test hook (LSB_SEQ_DENOM=1): always the sequential
+                           // denominator (softmax_denom.cuh)
 };
 
 // K5b: per-sentence top-B merge by (score desc, beam asc, word asc) +
@@ -144,7 +144,9 @@ struct SegArgs {
   int P;
   uint32_t seglen;
   float* part_max;    // [R][P]
-  double* part_sum;   // [R][P]
+  double* part_sum;   // [R][P] compensated segment sums: hi ...
+  double* part_c;     // [R][P] ... + compensation (hi + c = the exact sum up to 2^-60)
+  double* part_b;     // [R][P] sum_k min(e_k, 2^-52): bounds the sequential sum's error
   TopEntry* seg_top;  // [R][P][topB]
   int32_t* seg_n;     // [R][P]
   uint32_t* count;    // [R], zero between steps (self-resetting)
