@@ -147,6 +147,10 @@ class ClockSampler:
 
     def __enter__(self):
         if self.ok:
+            # the host loop that enqueues the steps holds the GIL between
+            # launches: a short switch interval lets the sampler run during it
+            self._switch = sys.getswitchinterval()
+            sys.setswitchinterval(0.0002)
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         return self
@@ -155,6 +159,7 @@ class ClockSampler:
         self._stop.set()
         if self.ok:
             self.t.join()
+            sys.setswitchinterval(self._switch)
 
     def summary(self):
         if not self.samples:
