@@ -3,7 +3,8 @@
 //
 //  K5a k_softmax_topb : one 128-thread CTA per hypothesis row. softmax_rows
 //      (src/beam_decoder.cpp:46-74): float max; e = exp((double)l - mx) kept
-//      as float(e); double denominator (a fixed-shape tree, so deterministic);
+//      as float(e); double denominator (a tree, certified equal to the
+//      reference's sequential sum or redone sequentially: softmax_denom.cuh);
 //      p = float(e) * float(1/denom). Then the row's top-B by (p desc, column
 //      asc): per-thread sorted lists (columns ascend within a thread, so equal
 //      p never displaces an earlier column) merged by B rounds of a block-wide
