@@ -60,6 +60,10 @@ struct lsb_batch {
   int fused_grid = 0, fused_rb = 0;
   uint32_t fused_slice_len = 0;  // probe slices: enough to cover the grid
   size_t fused_smem = 0;
+  int fused_timing = -1;                    // LSB_FUSED_TIMING (debug), read once
+  unsigned long long* fused_stamps = nullptr;  // mapped host memory [8]
+  double fused_acc[5] = {};
+  int fused_nacc = 0;
   // staging for lsb_step_host
   float* h_hidden = nullptr;
   double* h_scores = nullptr;

@@ -35,6 +35,7 @@ lsb_status free_batch(lsb_batch* b) {
                   b->split_cnt, b->split_arrive};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (b->fused_stamps) cudaFreeHost(b->fused_stamps);
   for (auto& sl : b->slot) {
     void* sp[] = {sl.hidden, sl.scores, sl.finished, sl.n_hyp, sl.choices, sl.n_choices};
     for (void* p : sp)

@@ -253,11 +253,16 @@ lsb_status launch_step_fused(lsb_batch* b, const lsb_state_dev* in, const lsb_ou
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  static unsigned long long* stamps = nullptr;  // debug: per-stage times
-  static double acc[5] = {};
-  static int nacc = 0;
-  if (getenv("LSB_FUSED_TIMING") && !stamps) cudaHostAlloc(&stamps, 8 * 8, cudaHostAllocMapped);
-  f.stamps = getenv("LSB_FUSED_TIMING") ? stamps : nullptr;
+  // LSB_FUSED_TIMING (debug): per-stage device times, mapped host stamps
+  // owned by the batch, averages printed every 200 steps
+  if (b->fused_timing < 0) b->fused_timing = getenv("LSB_FUSED_TIMING") != nullptr;
+  if (b->fused_timing && !b->fused_stamps &&
+      cudaHostAlloc(&b->fused_stamps, 8 * 8, cudaHostAllocMapped) != cudaSuccess) {
+    cudaGetLastError();
+    b->fused_stamps = nullptr;
+    b->fused_timing = 0;
+  }
+  f.stamps = b->fused_timing ? b->fused_stamps : nullptr;
   LSB_CUDA(cudaLaunchKernelEx(&cfg, kern, f));
   LSB_LAUNCHED(ctx, "k_step_fused");
   if (f.stamps) {
@@ -265,10 +270,13 @@ lsb_status launch_step_fused(lsb_batch* b, const lsb_state_dev* in, const lsb_ou
     cudaStreamIsCapturing(ctx->stream, &cs);
     if (cs != cudaStreamCaptureStatusNone) return *done = true, LSB_OK;
     LSB_CUDA(cudaStreamSynchronize(ctx->stream));
-    for (int k = 0; k < 5; ++k) acc[k] += (stamps[k + 1] - stamps[k]) * 1e-3;
-    if (++nacc % 200 == 0)
+    for (int k = 0; k < 5; ++k) b->fused_acc[k] += (f.stamps[k + 1] - f.stamps[k]) * 1e-3;
+    if (++b->fused_nacc % 200 == 0) {
+      const double* acc = b->fused_acc;
+      const int nacc = b->fused_nacc;
       fprintf(stderr, "k_step_fused stages (us): probe %.1f compact %.1f logits %.1f softmax %.1f expand %.1f\n",
               acc[0] / nacc, acc[1] / nacc, acc[2] / nacc, acc[3] / nacc, acc[4] / nacc);
+    }
   }
   *done = true;
   return LSB_OK;
