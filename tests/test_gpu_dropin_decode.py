@@ -25,7 +25,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SHIM = os.path.join(ROOT, "tests", "refsuite", "_build", "libdropin_shim.so")
 
 
-def run_decode(lib, V, d, seed, bias, K, u, W, beam, T, t, max_len, mode, eos):
+def run_decode(lib, V, d, seed, bias, K, u, W, beam, T, t, max_len, mode, eos, with_oracle=0):
     m = lib.ref_synth_model(V, d, seed, bias)
     assert m
     E = np.zeros((V, d), np.float32)
@@ -41,7 +41,7 @@ def run_decode(lib, V, d, seed, bias, K, u, W, beam, T, t, max_len, mode, eos):
         assert idx
     sp = np.array([eos], np.uint32)
     st = C.c_int(0)
-    h = lib.ref_decode(m, beam, T, t, max_len, sp, 1, mode, idx, 0, C.byref(st))
+    h = lib.ref_decode(m, beam, T, t, max_len, sp, 1, mode, idx, with_oracle, C.byref(st))
     assert h, lib.ref_last_error().decode()
     info = np.zeros(4, np.int32)
     prov = np.zeros(3, np.uint64)
@@ -55,13 +55,15 @@ def run_decode(lib, V, d, seed, bias, K, u, W, beam, T, t, max_len, mode, eos):
         lib.ref_decode_hyp(h, k, toks.ctypes.data, C.byref(score), C.byref(fin))
         hyps.append([toks[:n].tolist(), score.value.hex(), fin.value])
     vlsh = np.zeros(max(int(info[2]), 1), np.uint32)
-    lib.ref_decode_steps(h, vlsh.ctypes.data, None)
+    recall = np.zeros(max(int(info[3]), 1), np.float64)
+    lib.ref_decode_steps(h, vlsh.ctypes.data, recall.ctypes.data)
     lib.ref_decode_free(h)
     if idx:
         lib.ref_index_free(idx)
     lib.ref_model_free(m)
-    return dict(info=info[:3].tolist(), prov=prov.tolist(), hyps=hyps,
-                vlsh=vlsh[:int(info[2])].tolist())
+    return dict(info=info.tolist(), prov=prov.tolist(), hyps=hyps,
+                vlsh=vlsh[:int(info[2])].tolist(),
+                recall=[x.hex() for x in recall[:int(info[3])].tolist()])
 
 
 @pytest.fixture(scope="module")
@@ -97,6 +99,19 @@ CASES = [
     (2000, 32, 9, 3.0, 8, 3, 16, 12, 50, 2, 40, 1),      # long decode, frozen beams
     (2000, 32, 9, 3.0, 8, 3, 16, 12, 50, 2, 40, 0),
 ]
+
+
+@pytest.mark.parametrize("V,d,seed,bias,K,u,W,beam,T,t,max_len,mode", [CASES[0], CASES[3]])
+def test_decode_with_oracle_recall_equals_reference(ref_lib, V, d, seed, bias, K, u, W, beam, T,
+                                                    t, max_len, mode):
+    """decode(with_oracle=true): the per-step recall@B against the exact
+    full-vocabulary top-B (eval_oracle, src/eval_oracle.cpp:11-63; ours runs
+    it through lsb_exact_topb) is identical too."""
+    args = (V, d, seed, bias, K, u, W, beam, T, t, max_len, mode, V - 1, 1)
+    want = run_decode(ref_lib, *args)
+    got = ours_decode(args)
+    assert len(want["recall"]) > 0
+    assert got == want
 
 
 @pytest.mark.parametrize("V,d,seed,bias,K,u,W,beam,T,t,max_len,mode", CASES)
