@@ -234,7 +234,8 @@ __global__ void __launch_bounds__(1024) k_cuckoo_build(
     const uint32_t* __restrict__ elen, const uint32_t* __restrict__ n_entries, uint32_t V,
     unsigned long long index_seed, BandMeta* __restrict__ bands,
     unsigned long long* __restrict__ tmp, uint4* __restrict__ slots,
-    uint32_t* __restrict__ attempts_out, uint32_t* err, int sequential, int smem_cap) {
+    uint32_t* __restrict__ attempts_out, uint32_t* err, int sequential, int smem_cap,
+    int raw_seed) {
   __shared__ unsigned long long mul[2];
   __shared__ int fail;
   extern __shared__ __align__(16) unsigned long long sm_tab[];
@@ -255,7 +256,11 @@ __global__ void __launch_bounds__(1024) k_cuckoo_build(
     for (uint32_t e = threadIdx.x; e < ne; e += blockDim.x) sk[e] = ekey[off + e];
     keys = sk;
   }
-  unsigned long long g = mix_seed_dev(index_seed, static_cast<unsigned long long>(w));
+  // BandIndex::build seeds band w's table with mix_seed(seed, w)
+  // (src/band_index.cpp:90-132); a standalone CuckooTable::build(entries,
+  // seed) draws its multipliers from SplitMix64(seed) itself (:42-45)
+  unsigned long long g = raw_seed ? index_seed
+                                  : mix_seed_dev(index_seed, static_cast<unsigned long long>(w));
   for (int attempt = 0; attempt <= kMaxRebuilds; ++attempt) {
     if (threadIdx.x == 0) {
       mul[0] = sm64_next(g) | 1ull;
@@ -518,7 +523,7 @@ static lsb_status build_bands(lsb_ctx* ctx, lsb_index* idx, const uint32_t* code
   k_cuckoo_build<<<W, 1024, csmem, ctx->stream>>>(ekey.p, estart.p, elen.p, nent.p, V,
                                                   idx->index_seed, idx->bands, tmp.p, idx->slots,
                                                   attempts.p, ctx->err_dev,
-                                                  ctx->cuckoo_parallel ? 0 : 1, smem_cap);
+                                                  ctx->cuckoo_parallel ? 0 : 1, smem_cap, 0);
   LSB_LAUNCHED(ctx, "k_cuckoo_build");
   LSB_CUDA(cudaMemcpyAsync(idx->bands_host.data(), idx->bands, W * sizeof(BandMeta),
                            cudaMemcpyDeviceToHost, ctx->stream));
@@ -544,7 +549,7 @@ lsb_status build_cuckoo_band(lsb_ctx* ctx, const uint32_t* keys, const uint32_t*
                                            static_cast<int>(csmem)));
   k_cuckoo_build<<<1, 1024, csmem, ctx->stream>>>(keys, starts, lens, ne.p, n, seed, meta_dev, tmp.p,
                                                  slots_dev, attempts_dev, ctx->err_dev,
-                                                 ctx->cuckoo_parallel ? 0 : 1, smem_cap);
+                                                 ctx->cuckoo_parallel ? 0 : 1, smem_cap, 1);
   LSB_LAUNCHED(ctx, "k_cuckoo_build");
   return lsb_ctx_sync(ctx);
 }

@@ -1,0 +1,85 @@
+"""Seeded calls of the reference's public C++ API through the C wrapper
+oracle/ref_shim.cpp (oracle.oracle.Reference), for tests/test_gpu_dropin_api.py:
+run against the unmodified reference (oracle/_ref) and against our drop-in
+(the same wrapper compiled against include/lshbeam + liblshbeam.so), every
+returned array must be identical. Test infrastructure.
+
+  python tests/dropin_api_cases.py SHIM.so OUT.npz   (runs ours, saves arrays)
+"""
+import sys
+
+import numpy as np
+
+
+def run_all(R) -> dict:
+    out = {}
+    rng = np.random.default_rng(1234)
+    # rng / seeds (include/lshbeam/rng.hpp)
+    out["mix_seed"] = np.array([R.mix_seed(s, k) for s in (0, 7, 2**63 + 5) for k in (1, 2, 9)],
+                               np.uint64)
+    out["splitmix"] = R.splitmix(42, 64)
+    out["gaussian"] = R.gaussian(11, 4096)
+    # WTA (src/wta_hash.cpp)
+    for (d, K, u, W) in [(64, 8, 3, 16), (100, 4, 2, 20), (1000, 16, 3, 32), (600, 512, 1, 4)]:
+        perms = R.generate_perms(d, u * W, K, R.mix_seed(d, 1))
+        out[f"perms_{d}_{K}"] = perms
+        M = rng.standard_normal((50, d)).astype(np.float32)
+        M[3, :] = 0.0  # ties everywhere: the smallest index wins
+        out[f"hash_{d}_{K}_{u}_{W}"] = R.hash_matrix(M, K, u, W, perms=perms)
+        out[f"hash_seed_{d}_{K}_{u}_{W}"] = R.hash_matrix(M, K, u, W, seed=R.mix_seed(d, 1))
+    idx = rng.integers(0, 8, (16, 3)).astype(np.uint32)
+    out["pack_bands"] = R.pack_bands(idx.reshape(-1), 8, 3, 16)
+    # band index + cuckoo (src/band_index.cpp)
+    codes = rng.integers(0, 64, (3000, 16)).astype(np.uint32)
+    bt = R.band_index_build(codes, 99)
+    for k, v in bt._asdict().items() if hasattr(bt, "_asdict") else vars(bt).items():
+        if isinstance(v, (list, tuple)):
+            for i, a in enumerate(v):
+                out[f"bt_{k}_{i}"] = np.asarray(a)
+        else:
+            out[f"bt_{k}"] = np.asarray(v)
+    q = rng.integers(0, 64, (12, 16)).astype(np.uint32)
+    out["lookup_hits"] = R.lookup_hits_codes(codes, 99, q)
+    keys = np.unique(rng.integers(0, 2**31, 5000)).astype(np.uint32)
+    lg, muls, slots = R.cuckoo_build(keys, np.arange(len(keys), dtype=np.uint32),
+                                     np.ones(len(keys), np.uint32), 5)
+    out["cuckoo_lg"], out["cuckoo_muls"], out["cuckoo_slots"] = np.array([lg]), muls, slots
+    # candidates (src/candidate_selector.cpp)
+    L = rng.integers(0, 5, (12, 3000)).astype(np.int32)
+    for t in (0, 1, 2, 4):
+        ids, ft = R.select_candidates(L, t)
+        out[f"select_{t}"], out[f"select_ft_{t}"] = ids, np.array([ft])
+        m, prov = R.merge_top_frequent(ids, ft, 100, [2999, 5], 3000)
+        out[f"merge_{t}"], out[f"merge_prov_{t}"] = m, np.array(prov)
+    E = rng.standard_normal((3000, 100)).astype(np.float32)
+    ids = np.sort(rng.choice(3000, 400, replace=False)).astype(np.uint32)
+    Es = R.gather(E, ids)
+    out["gather"] = Es
+    H = rng.standard_normal((12, 100)).astype(np.float32)
+    logits = R.compute_logits(H, Es)
+    out["logits"] = logits
+    probs = R.softmax_rows(logits * 3.0)
+    out["probs"] = probs
+    cum = -rng.random(12) * 4
+    for B, frozen in [(12, ()), (5, ((-0.5, 3), (-9.0, 7))), (50, ())]:
+        s, b, w = R.expand_beams(probs, cum, np.arange(12, dtype=np.uint32), frozen, B, ids)
+        out[f"expand_s_{B}_{len(frozen)}"] = s
+        out[f"expand_b_{B}_{len(frozen)}"] = b
+        out[f"expand_w_{B}_{len(frozen)}"] = w
+    tids, tvals = R.exact_topb_logits(np.concatenate([logits, -np.abs(logits)]), 12)
+    out["topb_ids"], out["topb_vals"] = tids, tvals
+    # synthetic model (src/model_provider.cpp)
+    m = R.synth_model(500, 48, 21, 2.0)
+    for k, v in m.items():
+        out[f"model_{k}"] = v
+    return out
+
+
+if __name__ == "__main__":
+    sys.path.insert(0, sys.argv[3] if len(sys.argv) > 3 else ".")
+    from oracle.oracle import Reference
+    R = Reference(sys.argv[1])
+    res = run_all(R)
+    maps = open("/proc/self/maps").read()
+    assert "libref_lshbeam" not in maps and "liblshbeam.so" in maps
+    np.savez(sys.argv[2], **res)

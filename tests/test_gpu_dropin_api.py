@@ -1,0 +1,39 @@
+"""Drop-in conformance of the reference's public C++ API (include/lshbeam):
+the same seeded calls (tests/dropin_api_cases.py: seeds, WTA permutations and
+hashing incl. K=512, band packing, the band index and its cuckoo tables, hit
+lookup, threshold selection, top-frequent merge, gather, logits, softmax,
+beam expansion with frozen hypotheses, exact top-B, the synthetic model) go
+through the C wrapper oracle/ref_shim.cpp built once against the unmodified
+reference (oracle/_ref) and once against our liblshbeam.so
+(tests/refsuite/_build/libdropin_shim.so); every array must be identical, bit
+for bit. Ours runs in a process that never loads the reference library."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SHIM = os.path.join(ROOT, "tests", "refsuite", "_build", "libdropin_shim.so")
+
+
+def test_public_api_equals_reference(tmp_path):
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from dropin_api_cases import run_all
+    from oracle.oracle import Reference
+    if not (Reference.available() and os.path.exists(SHIM)):
+        pytest.skip("reference or drop-in shim not built")
+    want = run_all(Reference())
+    out = tmp_path / "ours.npz"
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "dropin_api_cases.py"), SHIM,
+                        str(out), ROOT], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    got = np.load(out)
+    assert sorted(got.files) == sorted(want)
+    bad = [k for k in want
+           if got[k].dtype != want[k].dtype or got[k].shape != want[k].shape
+           or got[k].tobytes() != want[k].tobytes()]
+    assert not bad, bad
