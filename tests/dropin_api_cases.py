@@ -68,10 +68,40 @@ def run_all(R) -> dict:
         out[f"expand_w_{B}_{len(frozen)}"] = w
     tids, tvals = R.exact_topb_logits(np.concatenate([logits, -np.abs(logits)]), 12)
     out["topb_ids"], out["topb_vals"] = tids, tvals
-    # synthetic model (src/model_provider.cpp)
+    # synthetic model (src/model_provider.cpp) and the recurrence
     m = R.synth_model(500, 48, 21, 2.0)
     for k, v in m.items():
         out[f"model_{k}"] = v
+    h = R.lib.ref_synth_model(2000, 1000, 7, 1.0)
+    x = np.zeros(1000, np.float32)
+    R.lib.ref_model_get(h, None, None, None, x.ctypes.data, None)
+    for k, tok in enumerate((5, 1999, 0, 77)):  # h' = tanh(W_h h + W_e emb[tok])
+        y = np.zeros(1000, np.float32)
+        R._chk(R.lib.ref_step_hidden(h, x, tok, y), "step_hidden")
+        out[f"step_hidden_{k}"] = y
+        x = y
+    R.lib.ref_model_free(h)
+    # build_lsh_index over embeddings (K1 on E + K2-build) and its lookups
+    E = R.gaussian(3, 4000 * 64).reshape(4000, 64)
+    ih = R.lib.ref_index_from_embeddings(E, 4000, 64, 8, 3, 16, R.mix_seed(3, 1), R.mix_seed(3, 2))
+    try:
+        bt = R._tables(ih, 4000, 16)
+        out["lsh_word_ids"], out["lsh_lg"] = bt.word_ids, bt.lg
+        out["lsh_mul"], out["lsh_slots"] = bt.mul, bt.slots
+    finally:
+        R.lib.ref_index_free(ih)
+    # one decode step body (kLsh / kFull) + expansion, src/beam_decoder.cpp:166-289
+    from oracle.oracle import ReferenceStepper
+    Hs = rng.standard_normal((12, 64)).astype(np.float32)
+    st = ReferenceStepper(R, E, R.gaussian(4, 4000) * 0.5, 8, 3, 16, R.mix_seed(3, 1),
+                          R.mix_seed(3, 2))
+    try:
+        for full in (False, True):
+            (s_, b_, w_), nc, _ = st.step(Hs, -rng.random(12) * 3, 12, 100, 2, [3999], full=full)
+            out[f"step_{full}_s"], out[f"step_{full}_b"], out[f"step_{full}_w"] = s_, b_, w_
+            out[f"step_{full}_n"] = np.array([nc])
+    finally:
+        st.close()
     return out
 
 

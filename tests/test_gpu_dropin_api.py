@@ -2,7 +2,8 @@
 the same seeded calls (tests/dropin_api_cases.py: seeds, WTA permutations and
 hashing incl. K=512, band packing, the band index and its cuckoo tables, hit
 lookup, threshold selection, top-frequent merge, gather, logits, softmax,
-beam expansion with frozen hypotheses, exact top-B, the synthetic model) go
+beam expansion with frozen hypotheses, exact top-B, the synthetic model and
+its recurrence, build_lsh_index over embeddings, one kLsh / kFull step) go
 through the C wrapper oracle/ref_shim.cpp built once against the unmodified
 reference (oracle/_ref) and once against our liblshbeam.so
 (tests/refsuite/_build/libdropin_shim.so); every array must be identical, bit
