@@ -90,6 +90,25 @@ def run_all(R) -> dict:
         out["lsh_mul"], out["lsh_slots"] = bt.mul, bt.slots
     finally:
         R.lib.ref_index_free(ih)
+    # error behaviour: which calls are rejected, and with which error class
+    def rejects(f, *a):
+        try:
+            f(*a)
+            return 0
+        except ValueError:
+            return 1
+        except RuntimeError:
+            return 2
+        except Exception:  # noqa: BLE001
+            return 3
+    out["rejects"] = np.array([
+        rejects(R.wta_params_check, 1, 3, 16), rejects(R.wta_params_check, 8, 0, 16),
+        rejects(R.wta_params_check, 8, 11, 16), rejects(R.wta_params_check, 8, 3, 0),
+        rejects(R.wta_params_check, 512, 3, 4), rejects(R.wta_params_check, 8, 3, 16),
+        rejects(R.generate_perms, 4, 6, 8, 1),
+        rejects(R.cuckoo_build, [0x7FFFFFFF], [0], [1], 1),
+        rejects(R.softmax_rows, np.full((1, 3), -np.inf, np.float32)),
+    ], np.int32)
     # one decode step body (kLsh / kFull) + expansion, src/beam_decoder.cpp:166-289
     from oracle.oracle import ReferenceStepper
     Hs = rng.standard_normal((12, 64)).astype(np.float32)
