@@ -25,7 +25,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SHIM = os.path.join(ROOT, "tests", "refsuite", "_build", "libdropin_shim.so")
 
 
-def run_decode(lib, V, d, seed, bias, K, u, W, beam, T, t, max_len, mode, eos, with_oracle=0):
+def run_decode(lib, V, d, seed, bias, K, u, W, beam, T, t, max_len, mode, eos, with_oracle=0,
+               eos_boost=0.0):
     m = lib.ref_synth_model(V, d, seed, bias)
     assert m
     E = np.zeros((V, d), np.float32)
@@ -34,6 +35,9 @@ def run_decode(lib, V, d, seed, bias, K, u, W, beam, T, t, max_len, mode, eos, w
     h0 = np.zeros(d, np.float32)
     b = np.zeros(V, np.float32)
     lib.ref_model_get(m, *[a.ctypes.data for a in (E, wh, we, h0, b)])
+    if eos_boost:  # model.eos_id = V - 1: raise its bias so beams finish early
+        b[V - 1] += np.float32(eos_boost)
+        lib.ref_model_set(m, None, b.ctypes.data)
     idx = None
     if mode != 0:
         idx = lib.ref_index_from_embeddings(E, V, d, K, u, W, lib.ref_mix_seed(seed, 1),
@@ -42,7 +46,11 @@ def run_decode(lib, V, d, seed, bias, K, u, W, beam, T, t, max_len, mode, eos, w
     sp = np.array([eos], np.uint32)
     st = C.c_int(0)
     h = lib.ref_decode(m, beam, T, t, max_len, sp, 1, mode, idx, with_oracle, C.byref(st))
-    assert h, lib.ref_last_error().decode()
+    if not h:  # rejected configuration: compare the status
+        if idx:
+            lib.ref_index_free(idx)
+        lib.ref_model_free(m)
+        return dict(rejected=st.value)
     info = np.zeros(4, np.int32)
     prov = np.zeros(3, np.uint64)
     stages = np.zeros(9, np.float64)
@@ -98,7 +106,30 @@ CASES = [
     (40000, 1000, 7, 1.0, 8, 3, 16, 12, 1000, 2, 4, 1),  # BASELINE cfg 1
     (2000, 32, 9, 3.0, 8, 3, 16, 12, 50, 2, 40, 1),      # long decode, frozen beams
     (2000, 32, 9, 3.0, 8, 3, 16, 12, 50, 2, 40, 0),
+    (2000, 32, 9, 3.0, 8, 3, 16, 1, 50, 2, 20, 1),       # greedy (beam 1)
+    (1500, 48, 4, 2.0, 8, 3, 16, 6, 1500, 2, 12, 1),     # T = V: every word is a candidate
+    (1500, 48, 4, 2.0, 8, 3, 16, 6, 20, 17, 12, 1),      # t > W: rejected by both
+    (1500, 48, 4, 2.0, 8, 3, 16, 6, 20, 16, 12, 1),      # t = W: few threshold survivors
 ]
+
+# the model's EOS (V - 1) with a raised bias: hypotheses finish at different
+# steps and the frozen-beam path of expand_beams carries them to the end
+EOS_CASES = [
+    (2000, 32, 13, 2.0, 8, 3, 16, 8, 50, 2, 30, 1),
+    (2000, 32, 13, 2.0, 8, 3, 16, 8, 50, 2, 30, 0),
+    (2000, 32, 13, 2.0, 8, 3, 16, 8, 50, 1, 30, 2),
+]
+
+
+@pytest.mark.parametrize("boost", [6.0, 9.0])
+@pytest.mark.parametrize("V,d,seed,bias,K,u,W,beam,T,t,max_len,mode", EOS_CASES)
+def test_decode_with_early_eos_equals_reference(ref_lib, V, d, seed, bias, K, u, W, beam, T, t,
+                                                max_len, mode, boost):
+    args = (V, d, seed, bias, K, u, W, beam, T, t, max_len, mode, V - 1, 0, boost)
+    want = run_decode(ref_lib, *args)
+    got = ours_decode(args)
+    assert any(h[2] for h in want["hyps"])  # some hypotheses finished
+    assert got == want
 
 
 @pytest.mark.parametrize("V,d,seed,bias,K,u,W,beam,T,t,max_len,mode", [CASES[0], CASES[3]])
@@ -119,6 +150,9 @@ def test_decode_equals_reference(ref_lib, V, d, seed, bias, K, u, W, beam, T, t,
     args = (V, d, seed, bias, K, u, W, beam, T, t, max_len, mode, V - 1)
     want = run_decode(ref_lib, *args)
     got = ours_decode(args)
+    if "rejected" in want:
+        assert "rejected" in got and (got["rejected"] != 0) == (want["rejected"] != 0)
+        return
     assert got["info"] == want["info"]
     assert got["prov"] == want["prov"]
     assert got["vlsh"] == want["vlsh"]
