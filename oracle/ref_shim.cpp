@@ -178,6 +178,32 @@ void* ref_index_from_embeddings(const float* E, uint32_t V, int d, int K, int u,
 
 void ref_index_free(void* h) { delete static_cast<RefIndex*>(h); }
 
+// WTAIDX1 / WTAEMB1 files (src/band_index.cpp:198-289,
+// src/model_provider.cpp:116-154): save an index built from embeddings, load
+// one back (the LshIndex round trip), save / load an embedding matrix.
+int ref_index_save(void* h, const char* path) {
+  return guarded([&] { save_lsh_index(*static_cast<RefIndex*>(h)->lsh, path); });
+}
+void* ref_index_load(const char* path) {
+  auto* h = new RefIndex;
+  const int rc = guarded([&] { h->lsh = std::make_unique<LshIndex>(load_lsh_index(path)); });
+  if (rc) { delete h; return nullptr; }
+  return h;
+}
+int ref_embeddings_save(const float* E, uint32_t V, int d, const char* path) {
+  return guarded([&] { save_embeddings(to_mat(E, V, d), path); });
+}
+int ref_embeddings_load(const char* path, float* E, uint64_t cap, uint32_t* V, int* d) {
+  return guarded([&] {
+    const MatF M = load_embeddings(path);
+    *V = static_cast<uint32_t>(M.rows());
+    *d = static_cast<int>(M.cols());
+    if (E && cap >= M.rows() * M.cols())
+      for (size_t i = 0; i < M.rows(); ++i)
+        std::memcpy(E + i * M.cols(), M.row(i).data(), M.cols() * sizeof(float));
+  });
+}
+
 int ref_index_band_words(void* h, int w, uint32_t* out) {
   const auto& b = static_cast<RefIndex*>(h)->b();
   auto s = b.band_words(w);

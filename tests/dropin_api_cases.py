@@ -132,3 +132,49 @@ if __name__ == "__main__":
     maps = open("/proc/self/maps").read()
     assert "libref_lshbeam" not in maps and "liblshbeam.so" in maps
     np.savez(sys.argv[2], **res)
+
+
+def index_tables(R, h, V, W):
+    bt = R._tables(h, V, W)
+    return {"word_ids": bt.word_ids, "lg": bt.lg, "mul": bt.mul, "slots": bt.slots}
+
+
+def write_files(R, d, tag):
+    """WTAIDX1 / WTAEMB1 files written by this library (src/band_index.cpp:198-289,
+    src/model_provider.cpp:116-154) for a seeded model and index."""
+    import ctypes as C
+    import os
+    lib = R.lib
+    lib.ref_index_save.argtypes = [C.c_void_p, C.c_char_p]
+    lib.ref_embeddings_save.argtypes = [C.c_void_p, C.c_uint32, C.c_int, C.c_char_p]
+    E = R.gaussian(5, 3000 * 40).reshape(3000, 40)
+    h = lib.ref_index_from_embeddings(E, 3000, 40, 8, 3, 16, R.mix_seed(5, 1), R.mix_seed(5, 2))
+    try:
+        R._chk(lib.ref_index_save(h, os.path.join(d, f"{tag}.idx").encode()), "save_lsh_index")
+    finally:
+        lib.ref_index_free(h)
+    R._chk(lib.ref_embeddings_save(E.ctypes.data, 3000, 40, os.path.join(d, f"{tag}.emb").encode()),
+           "save_embeddings")
+
+
+def read_files(R, d, tag):
+    """The other library's files read back: index tables and embeddings."""
+    import ctypes as C
+    import os
+    lib = R.lib
+    lib.ref_index_load.restype = C.c_void_p
+    lib.ref_index_load.argtypes = [C.c_char_p]
+    lib.ref_embeddings_load.argtypes = [C.c_char_p, C.c_void_p, C.c_uint64,
+                                        C.POINTER(C.c_uint32), C.POINTER(C.c_int)]
+    h = lib.ref_index_load(os.path.join(d, f"{tag}.idx").encode())
+    assert h, lib.ref_last_error().decode()
+    try:
+        out = {f"idx_{k}": v for k, v in index_tables(R, h, 3000, 16).items()}
+    finally:
+        lib.ref_index_free(h)
+    E = np.zeros((3000, 40), np.float32)
+    V, dd = C.c_uint32(), C.c_int()
+    R._chk(lib.ref_embeddings_load(os.path.join(d, f"{tag}.emb").encode(), E.ctypes.data, E.size,
+                                   C.byref(V), C.byref(dd)), "load_embeddings")
+    out["emb"], out["emb_shape"] = E, np.array([V.value, dd.value])
+    return out
