@@ -67,6 +67,16 @@ uint64_t mix64(uint64_t h, uint64_t v) {
   return h * 0xBF58476D1CE4E5B9ull;
 }
 
+// LSB_DROPIN_NO_CACHE=1: no device copies are reused across calls. The cache
+// key is (pointers, sizes, a content fingerprint that hashes matrices of up to
+// 2^18 floats entirely and samples larger ones), so a caller that edits a
+// large matrix in place between calls without changing those samples must set
+// it.
+bool no_device_cache() {
+  static const bool off = getenv("LSB_DROPIN_NO_CACHE") && atoi(getenv("LSB_DROPIN_NO_CACHE")) == 1;
+  return off;
+}
+
 // Content fingerprint of n floats (see cached_model).
 uint64_t fingerprint(const float* p, size_t n, size_t row) {
   if (!p) return 0;
@@ -108,6 +118,8 @@ std::shared_ptr<lsb_model> cached_model(const float* E, uint32_t vocab, int dim,
   // of construction, so the cached device copies are freed before it
   ctx();
   static std::vector<ModelEntry> cache;  // guarded by api_mutex (callers hold it)
+  if (no_device_cache())  // every call uploads (callers that mutate models in place)
+    return std::shared_ptr<lsb_model>(upload_model(E, vocab, dim, bias).release(), ModelDeleter{});
   const size_t n = static_cast<size_t>(vocab) * dim;
   const uint64_t fp = mix64(fingerprint(E, n, dim), fingerprint(bias, vocab, 0));
   for (size_t k = 0; k < cache.size(); ++k) {
@@ -126,6 +138,11 @@ std::shared_ptr<lsb_model> cached_model(const float* E, uint32_t vocab, int dim,
 std::shared_ptr<lsb_recurrent> cached_recurrent(const float* wh, const float* we, int dim) {
   ctx();  // constructed before the cache (see cached_model)
   static std::vector<RecEntry> cache;
+  if (no_device_cache()) {
+    lsb_recurrent* r = nullptr;
+    check(lsb_recurrent_create(ctx(), wh, we, dim, &r), "recurrent upload");
+    return std::shared_ptr<lsb_recurrent>(r, RecurrentDeleter{});
+  }
   const size_t n = static_cast<size_t>(dim) * dim;
   const uint64_t fp = mix64(fingerprint(wh, n, dim), fingerprint(we, n, dim));
   for (size_t k = 0; k < cache.size(); ++k) {
