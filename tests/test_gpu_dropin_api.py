@@ -38,3 +38,27 @@ def test_public_api_equals_reference(tmp_path):
            if got[k].dtype != want[k].dtype or got[k].shape != want[k].shape
            or got[k].tobytes() != want[k].tobytes()]
     assert not bad, bad
+
+
+MUTATE = """
+import sys; sys.path.insert(0, {root!r})
+import numpy as np
+from oracle.oracle import Reference
+R = Reference({shim!r})
+E = np.random.default_rng(0).standard_normal((2000, 1000)).astype(np.float32)
+a = R.gather(E, [5])
+E[5, 3] += 1.0  # an element the sampled content fingerprint does not read
+b = R.gather(E, [5])
+assert a[0, 3] != b[0, 3] and b[0, 3] == E[5, 3], (a[0, 3], b[0, 3], E[5, 3])
+"""
+
+
+def test_no_cache_sees_in_place_edits():
+    """LSB_DROPIN_NO_CACHE=1: a large matrix edited in place
+    between calls is re-read, as the reference reads host memory each call."""
+    if not os.path.exists(SHIM):
+        pytest.skip("drop-in shim not built")
+    r = subprocess.run([sys.executable, "-c", MUTATE.format(root=ROOT, shim=SHIM)],
+                       env={**os.environ, "LSB_DROPIN_NO_CACHE": "1"}, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
