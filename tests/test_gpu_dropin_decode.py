@@ -42,7 +42,9 @@ def run_decode(lib, V, d, seed, bias, K, u, W, beam, T, t, max_len, mode, eos, w
     if mode != 0:
         idx = lib.ref_index_from_embeddings(E, V, d, K, u, W, lib.ref_mix_seed(seed, 1),
                                             lib.ref_mix_seed(seed, 2))
-        assert idx
+        if not idx:  # invalid hash parameters: compare the rejection
+            lib.ref_model_free(m)
+            return dict(rejected=-1)
     sp = np.array([eos], np.uint32)
     st = C.c_int(0)
     h = lib.ref_decode(m, beam, T, t, max_len, sp, 1, mode, idx, with_oracle, C.byref(st))
@@ -157,3 +159,36 @@ def test_decode_equals_reference(ref_lib, V, d, seed, bias, K, u, W, beam, T, t,
     assert got["prov"] == want["prov"]
     assert got["vlsh"] == want["vlsh"]
     assert got["hyps"] == want["hyps"]
+
+
+def fuzz_cases(n=24, seed=2024):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        V = int(rng.integers(300, 5000))
+        d = int(rng.choice([8, 16, 33, 64, 100, 256]))
+        K = int(rng.choice([2, 4, 8, 16]))
+        K = min(K, d)
+        u = int(rng.integers(1, 4))
+        W = int(rng.integers(1, 40))
+        beam = int(rng.integers(1, 20))
+        T = int(rng.choice([0, int(rng.integers(1, V))]))
+        t = int(rng.integers(0, W + 1))
+        mode = int(rng.integers(0, 3))
+        out.append((V, d, int(rng.integers(0, 10**6)), float(rng.choice([0.0, 1.0, 4.0])), K, u, W,
+                    beam, T, t, int(rng.integers(1, 25)), mode, V - 1, 0,
+                    float(rng.choice([0.0, 5.0]))))
+    return out
+
+
+@pytest.mark.parametrize("args", fuzz_cases())
+def test_decode_fuzz_equals_reference(ref_lib, args):
+    """Random decode() configurations (vocabulary, dimension, hash shape, beam,
+    T, t, mode, length, bias, EOS bias): identical to the reference, or
+    rejected by both."""
+    want = run_decode(ref_lib, *args)
+    got = ours_decode(args)
+    if "rejected" in want:
+        assert "rejected" in got
+        return
+    assert got == want
