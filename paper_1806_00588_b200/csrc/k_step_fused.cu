@@ -13,6 +13,12 @@
 // so the 128-thread CTAs still cover the GPU; each slice counts its own word
 // range over all W bands, so the candidate sets do not depend on the split.
 //
+// Measured on B200 (S=1, B=12, cfg-1 shapes): 59 us per step against 37 us for
+// the separate kernels with PDL; its stages (probe 6.6, compact 8.7, logits
+// 14.7, softmax 7.2, expansion 17.3 us, grid barrier included) show the
+// one-CTA stages on 128 threads costing more than the launch gaps it removes.
+// Bit-exact with the separate kernels (tests/test_gpu_step.py), so opt-in.
+//
 // The device functions come from the kernels' own sources, included with
 // LSB_BODIES_ONLY (which hides their __global__ wrappers and host code):
 // whole-program compilation cannot call device code across files.
